@@ -1,0 +1,84 @@
+/* sb_attn.h — C ABI of the B200-native stick-breaking attention hot path.
+ *
+ * Drop-in boundary for the reference's tiled operator.
+ * Plain C types only; every call is stream-ordered, never synchronises the
+ * host, keeps no mutable global state (beyond one-time kernel attributes) and
+ * is bit-deterministic (no atomics on the data path).  The caller allocates
+ * every buffer, matching the reference's caller-owns-outputs convention
+ * (blocked.py:160-163, :250, :286-287).
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/pkg/src/sbattn/):
+ *   sb_fwd       blocked.py:129  blocked_forward(q, k, v, layout, skip, skip_eps,
+ *                                two_phase=True)  -> (o, RowLogAccumulator, TileStats)
+ *                blocked.py:218  sb_forward_blocked(q, k, v, layout, **kw)
+ *   sb_bwd       blocked.py:299  blocked_backward_twophase(cache, d_o, layout,
+ *                                row_offset)     -> (d_q, d_k, d_v, n_stored)
+ *   sb_snapshot_elems  blocked.py:58-60 BlockLayout.n_tiles x d_block (M/N size)
+ *   sb_status_string   the ValueError messages of blocked.py:115-119, :155-156,
+ *                      :246-247, :315-316, :398-399
+ */
+#ifndef SB_ATTN_H
+#define SB_ATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (0 = ok); non-zero mirror the reference's ValueError cases */
+enum {
+  SB_OK = 0,
+  SB_ERR_SHAPE = 1,        /* q/k/v/d_o shape or stride mismatch (blocked.py:116-119, :246) */
+  SB_ERR_SKIP_EPS = 2,     /* skip_eps outside (0, 1) (blocked.py:155-156) */
+  SB_ERR_BLOCK = 3,        /* d_block != 64 or seq_len < 1 (blocked.py:64-65) */
+  SB_ERR_UNSUPPORTED = 4,  /* head_dim not in {64, 128}, varlen, non-16B-aligned strides */
+  SB_ERR_NULL = 5,         /* required pointer is NULL (e.g. missing M, blocked.py:315-316) */
+  SB_ERR_DEVICE = 6,       /* no sm_100 device / driver entry point unavailable */
+  SB_ERR_LAUNCH = 7        /* CUDA launch or tensor-map encoding failed */
+};
+
+/* Problem description.  q, k, v, o, d_o, dq, dk, dv are bf16 with the element
+ * strides below and a contiguous last (head_dim) dimension, e.g. (B, H, L, d)
+ * contiguous: stride_b = H*L*d, stride_h = L*d, stride_l = d; or (B, L, H, d):
+ * stride_b = L*H*d, stride_l = H*d, stride_h = d. */
+typedef struct sb_params {
+  int32_t batch, heads, seqlen, head_dim;
+  int64_t stride_b, stride_h, stride_l;
+  const int32_t* cu_seqlens; /* reserved for packed varlen; must be NULL in this version */
+  float scale;               /* logit scale; 0 selects 1/sqrt(head_dim) (blocked.py:159) */
+  int32_t block;             /* skip / snapshot granularity; must be 64 (blocked.py:41) */
+  int32_t skip;              /* enable block skipping (blocked.py:175-176) */
+  float skip_eps;            /* in (0, 1); 0 selects 1e-6 (blocked.py:43) */
+} sb_params_t;
+
+/* Number of float elements of ONE snapshot array (M or N):
+ * batch * heads * n_tiles * 64 with n_tiles = nb*(nb+1)/2, nb = ceil(L/64). */
+size_t sb_snapshot_elems(const sb_params_t* p);
+
+/* Forward.  Outputs: o (bf16, q's layout), log_rem [B,H,L] float (natural log of
+ * the remaining stick mass, RowLogAccumulator.a), first_kb [B,H,nb] int32
+ * (TileStats.first_kb), M (snapshot array, opaque; required by sb_bwd),
+ * tile_counters (nullable) += {visited} (TileStats.visited).  stream is a
+ * cudaStream_t (NULL = legacy default stream). */
+int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, void* o,
+           float* log_rem, int32_t* first_kb, float* M, unsigned long long* tile_counters,
+           void* stream);
+
+/* Two-phase backward.  row_offset (nullable) [B,H,L] float is the per-row
+ * offset subtracted from dO.V^T (blocked.py:241-242, :274-276); N is a
+ * caller-provided snapshot workspace (sb_snapshot_elems floats).  Writes dq,
+ * dk, dv (bf16, q's layout). */
+int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
+           const float* row_offset, const float* log_rem, const int32_t* first_kb,
+           const float* M, float* N, void* dq, void* dk, void* dv, void* stream);
+
+const char* sb_status_string(int status);
+int sb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SB_ATTN_H */

@@ -1,0 +1,148 @@
+// C-ABI entry points (include/sb_attn.h): validation mirroring the reference's
+// ValueErrors, TMA tensor-map encoding and kernel dispatch.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "../../include/sb_attn.h"
+#include "sb_args.cuh"
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 4-D map over (d, L, H, B) of a bf16 tensor; box = 64 columns x rows.
+int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
+  auto fn = encode_fn();
+  if (!fn) return SB_ERR_DEVICE;
+  const cuuint64_t dims[4] = {(cuuint64_t)p->head_dim, (cuuint64_t)p->seqlen,
+                              (cuuint64_t)p->heads, (cuuint64_t)p->batch};
+  // strides of singleton dimensions are never dereferenced; keep them legal
+  auto legal = [](int64_t s_el, int n, int64_t fallback) -> cuuint64_t {
+    int64_t s = s_el * 2;
+    if (n == 1 && (s <= 0 || s % 16)) s = fallback;
+    return (cuuint64_t)s;
+  };
+  const int64_t fb = (int64_t)p->head_dim * 2 * 16;
+  const cuuint64_t strides[3] = {legal(p->stride_l, p->seqlen, fb), legal(p->stride_h, p->heads, fb),
+                                 legal(p->stride_b, p->batch, fb)};
+  const cuuint32_t box[4] = {64, (cuuint32_t)rows, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SB_OK : SB_ERR_LAUNCH;
+}
+
+int validate(const sb_params_t* p) {
+  if (!p) return SB_ERR_NULL;
+  if (p->cu_seqlens) return SB_ERR_UNSUPPORTED;
+  if (p->block != 64) return SB_ERR_BLOCK;
+  if (p->seqlen < 1 || p->batch < 1 || p->heads < 1) return SB_ERR_BLOCK;
+  if (p->head_dim != 64 && p->head_dim != 128) return SB_ERR_UNSUPPORTED;
+  if (p->skip && !(p->skip_eps == 0.0f || (p->skip_eps > 0.0f && p->skip_eps < 1.0f)))
+    return SB_ERR_SKIP_EPS;
+  for (int64_t s : {p->stride_l, p->stride_h, p->stride_b})
+    if (s < 0) return SB_ERR_SHAPE;
+  if ((p->stride_l * 2) % 16 || (p->heads > 1 && (p->stride_h * 2) % 16) ||
+      (p->batch > 1 && (p->stride_b * 2) % 16))
+    return SB_ERR_UNSUPPORTED;
+  return SB_OK;
+}
+
+sb::Geom geom(const sb_params_t* p) {
+  sb::Geom g;
+  g.B = p->batch;
+  g.H = p->heads;
+  g.L = p->seqlen;
+  g.nb = (p->seqlen + 63) / 64;
+  g.n_qt = (p->seqlen + 127) / 128;
+  g.n_tiles = (int64_t)g.nb * (g.nb + 1) / 2;
+  const float scale = p->scale != 0.0f ? p->scale : (float)(1.0 / std::sqrt((double)p->head_dim));
+  g.scale_log2 = scale * sb::kLog2e;
+  g.sb = p->stride_b;
+  g.sh = p->stride_h;
+  g.sl = p->stride_l;
+  return g;
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+size_t sb_snapshot_elems(const sb_params_t* p) {
+  if (!p || p->seqlen < 1) return 0;
+  const size_t nb = (size_t)(p->seqlen + 63) / 64;
+  return (size_t)p->batch * p->heads * (nb * (nb + 1) / 2) * 64;
+}
+
+int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, void* o,
+           float* log_rem, int32_t* first_kb, float* M, unsigned long long* tile_counters,
+           void* stream) {
+  int st = validate(p);
+  if (st) return st;
+  if (!q || !k || !v || !o || !log_rem || !first_kb || !M) return SB_ERR_NULL;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return SB_ERR_UNSUPPORTED;
+  CUtensorMap tq, tk, tv;
+  if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tk, k, p, 64)) ||
+      (st = make_map(&tv, v, p, 64)))
+    return st;
+  sb::FwdArgs a;
+  a.g = geom(p);
+  a.o = reinterpret_cast<__nv_bfloat16*>(o);
+  a.log_rem = log_rem;
+  a.first_kb = first_kb;
+  a.M = M;
+  a.counters = tile_counters;
+  const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
+  a.log_eps = std::log(eps);
+  int rc = sb::fwd_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a,
+                            reinterpret_cast<cudaStream_t>(stream));
+  return rc ? SB_ERR_LAUNCH : SB_OK;
+}
+
+int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
+           const float* row_offset, const float* log_rem, const int32_t* first_kb,
+           const float* M, float* N, void* dq, void* dk, void* dv, void* stream) {
+  int st = validate(p);
+  if (st) return st;
+  (void)q; (void)k; (void)v; (void)d_o; (void)row_offset; (void)log_rem; (void)first_kb;
+  (void)M; (void)N; (void)dq; (void)dk; (void)dv; (void)stream;
+  return SB_ERR_UNSUPPORTED;
+}
+
+const char* sb_status_string(int s) {
+  switch (s) {
+    case SB_OK: return "ok";
+    case SB_ERR_SHAPE: return "q, k, v (and d_o) must share one layout and shape";
+    case SB_ERR_SKIP_EPS: return "skip_eps must be in (0, 1)";
+    case SB_ERR_BLOCK: return "seq_len, batch, heads must be >= 1 and d_block must be 64";
+    case SB_ERR_UNSUPPORTED: return "unsupported configuration (head_dim must be 64 or 128, "
+                                    "16-byte aligned rows and strides, no varlen)";
+    case SB_ERR_NULL: return "required pointer is NULL (two-phase backward needs M snapshots)";
+    case SB_ERR_DEVICE: return "CUDA driver entry point unavailable (no sm_100 device?)";
+    case SB_ERR_LAUNCH: return "CUDA launch failed";
+    default: return "unknown status";
+  }
+}
+
+int sb_version(void) { return 1; }
+
+}  // extern "C"

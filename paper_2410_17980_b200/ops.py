@@ -1,0 +1,272 @@
+"""Host-side mirror of the reference's tiled operator, over the C-ABI CUDA library.
+
+Reference surface (/root/reference/pkg/src/sbattn/blocked.py) and its
+counterparts here:
+
+=================================  ==========================================
+reference                          this module
+=================================  ==========================================
+``plan_blocks`` / ``BlockLayout``  ``plan_blocks`` / ``BlockLayout`` (:46-67)
+``TileStats`` / ``skip_stats``     ``TileStats`` / ``skip_stats`` (:82-103)
+``default_skip_eps``               ``default_skip_eps`` (bf16 -> 1e-6, :106-107)
+``blocked_forward(two_phase)``     ``blocked_forward`` -> (o, log_rem, stats, cache)
+``blocked_backward_twophase``      ``blocked_backward_twophase(cache, d_o, row_offset)``
+``sb_forward_blocked``             ``sb_forward_blocked``
+(paper's upstream operator)        ``stickbreaking_attention(q, k, v, ...)`` autograd op
+=================================  ==========================================
+
+Tensors are CUDA bf16 of shape (B, H, L, d) (any strides with a contiguous last
+dim; q, k, v share one layout).  Unlike the reference (one L x d head per call)
+every call covers all (batch, head) units at once.  Errors the reference raises
+as ValueError are raised as ValueError here.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+DEFAULT_BLOCK = 64
+SKIP_EPS_BF16 = 1e-6  # the reference's f32 default (blocked.py:43) is used for bf16
+
+
+@dataclass(frozen=True)
+class BlockLayout:
+    """blocked.py:46-60 restated."""
+
+    seq_len: int
+    block: int
+    n_blocks: int
+    tail: int
+
+    def span(self, b: int) -> tuple[int, int]:
+        lo = b * self.block
+        return lo, min(lo + self.block, self.seq_len)
+
+    @property
+    def n_tiles(self) -> int:
+        return self.n_blocks * (self.n_blocks + 1) // 2
+
+
+def plan_blocks(seq_len: int, d_block: int = DEFAULT_BLOCK) -> BlockLayout:
+    """blocked.py:63-67 restated (ValueError on seq_len < 1 or d_block < 1)."""
+    if seq_len < 1 or d_block < 1:
+        raise ValueError("seq_len and d_block must be >= 1")
+    n_blocks = -(-seq_len // d_block)
+    return BlockLayout(seq_len, d_block, n_blocks, seq_len % d_block)
+
+
+@dataclass
+class TileStats:
+    """blocked.py:82-88; totals are over all (batch, head) units of the call."""
+
+    total: int
+    visited: int
+    skipped: int
+    first_kb: torch.Tensor  # (B, H, n_blocks) int32, leftmost visited key block
+
+
+def skip_stats(stats: TileStats) -> tuple[int, int, float]:
+    """blocked.py:101-103."""
+    return stats.visited, stats.skipped, stats.skipped / stats.total
+
+
+def default_skip_eps(dtype) -> float:
+    """blocked.py:106-107: f64 -> 1e-12, otherwise the f32 default 1e-6."""
+    return 1e-12 if dtype == torch.float64 else SKIP_EPS_BF16
+
+
+@dataclass
+class BlockedCache:
+    """blocked.py:90-98 analogue: what the two-phase backward needs."""
+
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    scale: float
+    layout: BlockLayout
+    log_rem: torch.Tensor
+    first_kb: torch.Tensor
+    M: torch.Tensor
+    skip: bool
+    skip_eps: float
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check_qkv(q, k, v):
+    if not (q.shape == k.shape == v.shape):
+        raise ValueError("q, k, v must share one shape")  # blocked.py:116-117
+    if q.dim() != 4:
+        raise ValueError("q, k, v must be (batch, heads, seq_len, head_dim)")
+    for t in (q, k, v):
+        if not t.is_cuda:
+            raise RuntimeError("stickbreaking_attention: CUDA tensors required (no CPU fallback)")
+        if t.dtype != torch.bfloat16:
+            raise TypeError("stickbreaking_attention: bf16 tensors required")
+    if q.shape[-1] not in (64, 128):
+        raise ValueError(f"head_dim {q.shape[-1]} unsupported (64 or 128)")
+
+
+def _same_layout(*ts):
+    base = ts[0]
+    if base.stride(-1) != 1 or base.data_ptr() % 16:
+        base = base.contiguous()
+    out = [base]
+    for t in ts[1:]:
+        out.append(t if (t.stride() == base.stride() and t.data_ptr() % 16 == 0)
+                   else t.contiguous() if base.is_contiguous() else
+                   torch.empty_like(base).copy_(t))
+    return out
+
+
+def _params(q, scale, skip, skip_eps, block=DEFAULT_BLOCK) -> _lib.SbParams:
+    B, H, L, d = q.shape
+    sb, sh, sl, sd = q.stride()
+    p = _lib.SbParams()
+    p.batch, p.heads, p.seqlen, p.head_dim = B, H, L, d
+    p.stride_b, p.stride_h, p.stride_l = sb, sh, sl
+    p.cu_seqlens = None
+    p.scale = float(scale)
+    p.block = block
+    p.skip = int(bool(skip))
+    p.skip_eps = float(skip_eps)
+    return p
+
+
+def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = False,
+                    skip_eps: float | None = None, scale: float | None = None,
+                    counters: bool = True):
+    """blocked_forward(two_phase=True) over every (b, h) unit (blocked.py:129-206).
+
+    Returns (o, log_rem, TileStats, BlockedCache).  log_rem is the reference's
+    RowLogAccumulator.a (natural log of the remaining stick mass).
+    """
+    _check_qkv(q, k, v)
+    B, H, L, d = q.shape
+    if layout is None:
+        layout = plan_blocks(L)
+    if layout.seq_len != L:
+        raise ValueError(f"layout is for L={layout.seq_len}, inputs have L={L}")  # :118-119
+    if layout.block != DEFAULT_BLOCK:
+        raise ValueError("the CUDA path runs d_block = 64 (blocked.py:41)")
+    if skip_eps is None:
+        skip_eps = default_skip_eps(q.dtype)
+    if not 0.0 < skip_eps < 1.0:
+        raise ValueError("skip_eps must be in (0, 1)")  # blocked.py:155-156
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    q, k, v = _same_layout(q, k, v)
+    lib = _lib.load()
+    p = _params(q, scale, skip, skip_eps)
+    o = torch.empty_like(q)
+    log_rem = torch.empty((B, H, L), device=q.device, dtype=torch.float32)
+    first_kb = torch.empty((B, H, layout.n_blocks), device=q.device, dtype=torch.int32)
+    M = torch.empty(lib.sb_snapshot_elems(ctypes.byref(p)), device=q.device, dtype=torch.float32)
+    cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
+    _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
+                          _ptr(first_kb), _ptr(M), _ptr(cnt), _stream()))
+    total = B * H * layout.n_tiles
+    visited = int(cnt[0].item()) if counters else -1
+    stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
+    cache = BlockedCache(q, k, v, scale, layout, log_rem, first_kb, M, skip, skip_eps)
+    return o, log_rem, stats, cache
+
+
+def sb_forward_blocked(q, k, v, layout=None, **kw):
+    """blocked.py:218-226: (o, cache) convenience wrapper."""
+    o, _, _, cache = blocked_forward(q, k, v, layout, **kw)
+    return o, cache
+
+
+def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | None = None,
+                              row_offset=None):
+    """blocked_backward_twophase (blocked.py:299-392) over every (b, h) unit.
+
+    Returns (d_q, d_k, d_v, n_stored_tiles).  row_offset (B, H, L) float32 is
+    subtracted from dO.V^T per query row (blocked.py:241-242).
+    """
+    if layout is not None and layout != cache.layout:
+        raise ValueError("layout does not match the one the cache was built with")
+    if cache.M is None:
+        raise ValueError("two-phase backward needs a forward run with two_phase=True "
+                         "(M snapshots missing)")
+    q, k, v = cache.q, cache.k, cache.v
+    if d_o.shape != v.shape:
+        raise ValueError("d_o shape mismatch")
+    if d_o.dtype != torch.bfloat16 or not d_o.is_cuda:
+        raise TypeError("d_o must be a CUDA bf16 tensor")
+    if d_o.stride() != q.stride() or d_o.data_ptr() % 16:
+        d_o = torch.empty_like(q).copy_(d_o)
+    lib = _lib.load()
+    p = _params(q, cache.scale, cache.skip, cache.skip_eps)
+    N = torch.empty_like(cache.M)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    ro = None
+    if row_offset is not None:
+        ro = row_offset.to(device=q.device, dtype=torch.float32).contiguous()
+        if ro.shape != cache.log_rem.shape:
+            raise ValueError("row_offset must be (batch, heads, seq_len)")
+    _lib.check(lib.sb_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
+                          _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M), _ptr(N),
+                          _ptr(dq), _ptr(dk), _ptr(dv), _stream()))
+    return dq, dk, dv, cache.layout.n_tiles * q.shape[0] * q.shape[1]
+
+
+class _StickBreakingFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, scale, skip, skip_eps):
+        o, log_rem, _, cache = blocked_forward(q, k, v, skip=skip, skip_eps=skip_eps,
+                                               scale=scale, counters=False)
+        ctx.cache = cache
+        ctx.save_for_backward(cache.q, cache.k, cache.v, cache.log_rem, cache.first_kb, cache.M)
+        rem = torch.exp(log_rem)
+        ctx.mark_non_differentiable(log_rem)
+        return o, rem
+
+    @staticmethod
+    def backward(ctx, d_o, d_rem):
+        q, k, v, log_rem, first_kb, M = ctx.saved_tensors
+        c = ctx.cache
+        cache = BlockedCache(q, k, v, c.scale, c.layout, log_rem, first_kb, M, c.skip, c.skip_eps)
+        if d_o is None:
+            d_o = torch.zeros_like(q)
+        # rem_j = 1 - sum_i A_ij  =>  dL/dA_ij -= dL/drem_j : the reference's
+        # row_offset hook (blocked.py:241-242, model.py:227-230)
+        dq, dk, dv, _ = blocked_backward_twophase(cache, d_o.to(torch.bfloat16), row_offset=d_rem)
+        return dq, dk, dv, None, None, None
+
+
+def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool = False,
+                            skip_eps: float | None = None, return_rem: bool = False,
+                            attend_current: bool = False):
+    """Stick-breaking attention (arXiv 2410.17980), strictly causal.
+
+    q, k, v: CUDA bf16 (batch, heads, seq_len, head_dim), head_dim 64 or 128.
+    o_j = sum_{i<j} A_ij v_i with A_ij = sigma(z_ij) prod_{i<k<j} (1 - sigma(z_kj)),
+    z = q k^T * scale (scale defaults to 1/sqrt(head_dim)).  With return_rem the
+    remaining stick mass rem_j = 1 - sum_i A_ij (B, H, L) float32 is returned too
+    and is differentiable.  skip enables the reference's block skipping
+    (exact: a skipped block's weights are below skip_eps).
+    """
+    if attend_current:
+        raise ValueError("attend_current=True is not part of the reference semantics "
+                         "(strict causality, attention.py:52-54)")
+    _check_qkv(q, k, v)
+    if skip_eps is None:
+        skip_eps = SKIP_EPS_BF16
+    if scale is None:
+        scale = 1.0 / math.sqrt(q.shape[-1])
+    o, rem = _StickBreakingFn.apply(q, k, v, float(scale), bool(skip), float(skip_eps))
+    return (o, rem) if return_rem else o
