@@ -123,9 +123,27 @@ int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, co
            const float* M, float* N, void* dq, void* dk, void* dv, void* stream) {
   int st = validate(p);
   if (st) return st;
-  (void)q; (void)k; (void)v; (void)d_o; (void)row_offset; (void)log_rem; (void)first_kb;
-  (void)M; (void)N; (void)dq; (void)dk; (void)dv; (void)stream;
-  return SB_ERR_UNSUPPORTED;
+  (void)log_rem;  // the backward reads the per-tile M snapshots, not the final a
+  if (!q || !k || !v || !d_o || !first_kb || !N || !dq || !dk || !dv) return SB_ERR_NULL;
+  if (!M) return SB_ERR_NULL;  // blocked.py:315-316: M snapshots missing
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(d_o) || !aligned16(dq) ||
+      !aligned16(dk) || !aligned16(dv))
+    return SB_ERR_UNSUPPORTED;
+  CUtensorMap tq, tdo, tk, tv;
+  if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
+      (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)))
+    return st;
+  sb::BwdArgs a;
+  a.g = geom(p);
+  a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
+  a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+  a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+  a.row_offset = row_offset;
+  a.first_kb = first_kb;
+  a.M = M;
+  a.N = N;
+  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, a, reinterpret_cast<cudaStream_t>(stream));
+  return rc ? SB_ERR_LAUNCH : SB_OK;
 }
 
 const char* sb_status_string(int s) {

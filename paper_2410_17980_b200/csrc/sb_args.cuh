@@ -14,6 +14,19 @@ struct FwdArgs {
   double log_eps;        // log(skip_eps)
 };
 
+struct BwdArgs {
+  Geom g;
+  __nv_bfloat16* dq;
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  const float* row_offset;  // [B,H,L] or null
+  const int32_t* first_kb;  // [B,H,nb] from the forward
+  const float* M;           // forward snapshots (log2 units)
+  float* N;                 // phase-1 b snapshots, read by phase 2
+};
+
+int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
+                 const CUtensorMap& tv, const BwdArgs& a, cudaStream_t stream);
 int fwd_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
                  const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
 
