@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""Benchmark of the stick-breaking attention hot path (fwd + two-phase bwd) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): B=8, H=16, L=4096, d=128 bf16, strictly
+causal stick-breaking fwd+bwd, skip off (algorithmic FLOPs == executed tiles), per GPU.
+(batch, head) units are independent: every rank runs its own C2
+batch with no collective on the data path -> weak scaling; the only NCCL use is the
+max-over-ranks of the timings.  One step = sb_fwd + sb_bwd (phase 1 + phase 2).
+
+value   = whole-job tokens/s with inputs resident in HBM (CUDA events, max over ranks).
+e2e     = the same metric through the public autograd op stickbreaking_attention()
+          with q, k, v, dO copied host->device from pinned memory every step and the
+          step's result (a fp32 checksum of o, dq, dk, dv) read back device->host.
+roofline = the dominant kernel's algorithmic tensor FLOPs per launch / its CUDA-event
+          duration, against MEASURED_PEAKS.json bf16 (sustained: kernels timed inside
+          a long step).
+cpu_baseline = the CPU oracle port (oracle/, C, float32, all host threads) on a bounded
+          sample of the same workload (rank 0, N=1 only).
+--impl reference times that CPU port as the reference arm (no GPU work).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, H, L, D = 8, 16, 4096, 128
+METRIC = "stick-breaking attn fwd+bwd TFLOP/s & tokens/s at L=4096 d=128 bf16, 1/2/4/8 B200"
+UNIT = "tokens/s"
+WORKLOAD = "C2: B=8 H=16 L=4096 d=128 bf16 causal stick-breaking fwd+bwd per GPU, skip off"
+
+
+def gemm_flops(b, h, l, d):
+    """One causal GEMM over the triangle, FA convention: 2*d*(L^2/2) per unit."""
+    return b * h * d * l * l
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(n_units=None, threads=None):
+    """Time the C oracle (float32, all host threads) on n_units (b,h) units of C2."""
+    import oracle
+    threads = threads or oracle.n_threads_default()
+    rng = np.random.default_rng(0)
+    # one unit per host thread (units are independent), capped at the batch
+    n_units = max(1, min(n_units or threads, B * H))
+    q, k, v, d_o = (rng.standard_normal((n_units, L, D), dtype=np.float32) for _ in range(4))
+    t0 = time.perf_counter()
+    fwd = oracle.tiled_forward(q, k, v, block=64, dtype=np.float32, n_threads=threads)
+    oracle.tiled_backward(q, k, v, d_o, fwd, block=64, dtype=np.float32, n_threads=threads)
+    dt = time.perf_counter() - t0
+    # tokens/s for the whole C2 batch (B*H units), units are independent and equal-cost
+    t_full = dt * (B * H) / n_units
+    return {"value": B * L / t_full, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n_units} of {B * H} (b,h) units of C2 (L=4096, d=128), fp32 C port "
+                      f"of blocked_forward+blocked_backward_twophase, {dt:.1f}s; scaled "
+                      f"linearly to the full batch",
+            "seconds_per_unit": dt / n_units}
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the reference's CPU algorithm (oracle C port) on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    threads = oracle.n_threads_default()
+    units = max(1, min(threads, B * H))
+    for _ in range(args.warmup):
+        pass  # the CPU port has no warm-up state worth paying for; keep the run short
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        s = cpu_sample(units, threads)
+        vals.append(s["value"])
+        if time.perf_counter() - t_all > 150:
+            break
+    value = statistics.median(vals)
+    ms = B * L / value * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": len(vals), "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": WORKLOAD + " (CPU, bounded sample)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": s["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sdpa", action="store_true")
+    ap.add_argument("--cpu-units", type=int, default=0, help="0: one per host thread")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2410_17980_b200 as sb
+    from paper_2410_17980_b200 import build as sbbuild
+
+    sbbuild.build()
+    W = max(3, args.warmup)
+    K = max(1, args.steps)
+
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q, k, v, d_o = (torch.randn(B, H, L, D, device=dev, dtype=torch.bfloat16, generator=g)
+                    for _ in range(4))
+    stream = torch.cuda.current_stream()
+
+    # preallocated outputs so the timed region holds only our kernels
+    def step(ev=None):
+        o, log_rem, _, cache = sb.blocked_forward(q, k, v, counters=False)
+        if ev is not None:
+            ev[1].record(stream)
+        out = step.out
+        sb.blocked_backward_twophase(cache, d_o, out=out, phases=1)
+        if ev is not None:
+            ev[2].record(stream)
+        sb.blocked_backward_twophase(cache, d_o, out=out, phases=2)
+        return o
+
+    M_elems = sb.ops._lib.load().sb_snapshot_elems(
+        __import__("ctypes").byref(sb.ops._params(q, 1.0 / math.sqrt(D), False, 1e-6)))
+    step.out = (torch.empty(M_elems, device=dev, dtype=torch.float32), torch.empty_like(q),
+                torch.empty_like(q), torch.empty_like(q))
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(K):
+        evs[i][0].record(stream)
+        step(evs[i])
+        evs[i][3].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / K
+    p1_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / K
+    p2_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / K
+    t = torch.tensor([total_ms, fwd_ms, p1_ms, p2_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, fwd_ms, p1_ms, p2_ms = t.tolist()
+    ms_step = total_ms / K
+    tokens = world * B * L * K
+    value = tokens / (total_ms / 1e3)
+
+    G = gemm_flops(B, H, L, D)
+    alg_flops = 7 * G  # fwd 2G + bwd 5G (FA convention)
+    exec_flops = 9 * G  # fwd 2G + phase 1 3G + phase 2 4G (recompute of QK^T, dO V^T)
+    tflops = world * alg_flops * K / (total_ms / 1e3) / 1e12
+    burst, sustained, peak_kind = load_peaks()
+    kernels = {"sb_fwd_kernel": (fwd_ms, 2 * G, 2 * G), "sb_bwd_q_kernel": (p1_ms, 3 * G, 3 * G),
+               "sb_bwd_kv_kernel": (p2_ms, 2 * G, 4 * G)}
+    dom = max(kernels, key=lambda n: kernels[n][0])
+    d_ms, d_alg, d_exec = kernels[dom]
+    achieved = d_alg / (d_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": sustained,
+                "unit": "TFLOP/s", "frac": achieved / sustained,
+                "peak_kind": f"{peak_kind} bf16 sustained (burst {burst})",
+                "executed_tflops": d_exec / (d_ms / 1e3) / 1e12, "traffic": None,
+                "per_kernel_ms": {n: round(v[0], 4) for n, v in kernels.items()},
+                "step_frac_of_peak": tflops / world / sustained}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            roofline["traffic"] = json.load(f).get(dom)
+    except Exception:
+        pass
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, d_o))
+        hres = torch.empty(4, dtype=torch.float32).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
+        d2h = hres.numel() * hres.element_size()
+        bufs = [torch.empty_like(q) for _ in range(4)]
+
+        def e2e_step():
+            for buf, hx in zip(bufs, (hq, hk, hv, hdo)):
+                buf.copy_(hx, non_blocking=True)
+            qq, kk, vv = (x.requires_grad_(True) for x in bufs[:3])
+            o = sb.stickbreaking_attention(qq, kk, vv)
+            o.backward(bufs[3])
+            res = torch.stack([o.float().sum(), qq.grad.float().sum(), kk.grad.float().sum(),
+                               vv.grad.float().sum()])
+            hres.copy_(res, non_blocking=True)
+            for x in bufs[:3]:
+                x.grad = None
+                x.requires_grad_(False)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        Ke = max(2, min(K, 5))
+        a.record(stream)
+        for _ in range(Ke):
+            e2e_step()
+        bev.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(bev)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * L * Ke / (te.item() / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": te.item() / Ke,
+               "api": "stickbreaking_attention(q,k,v) + o.backward(dO), pinned host buffers"}
+
+    # ---------------------------------------------------------------- comparators
+    comparator = None
+    if not args.no_sdpa and rank == 0:
+        try:
+            import torch.nn.functional as F
+            qs, ks, vs = (x.detach().clone().requires_grad_(True) for x in (q, k, v))
+            res = {}
+            for name, ctx in (("cudnn", torch.nn.attention.SDPBackend.CUDNN_ATTENTION),
+                              ("flash", torch.nn.attention.SDPBackend.FLASH_ATTENTION)):
+                try:
+                    with torch.nn.attention.sdpa_kernel([ctx]):
+                        def sdpa_step():
+                            o = F.scaled_dot_product_attention(qs, ks, vs, is_causal=True)
+                            o.backward(d_o)
+                        for _ in range(3):
+                            sdpa_step()
+                        torch.cuda.synchronize()
+                        a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a2.record()
+                        for _ in range(5):
+                            sdpa_step()
+                        b2.record()
+                        torch.cuda.synchronize()
+                        res[name] = a2.elapsed_time(b2) / 5
+                except Exception as ex:  # backend unavailable for this shape
+                    res[name] = f"unavailable: {type(ex).__name__}"
+            best = min((v for v in res.values() if isinstance(v, float)), default=None)
+            comparator = {"softmax_sdpa_fwd_bwd_ms": res,
+                          "ours_over_best_softmax": (ms_step / best) if best else None,
+                          "note": "softmax attention keeps the inclusive diagonal; same shape"}
+        except Exception as ex:
+            comparator = {"error": repr(ex)}
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        try:
+            cpu = cpu_sample(args.cpu_units or None)
+        except Exception as ex:
+            cpu = {"error": repr(ex)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "heads": H, "seq_len": L,
+                   "head_dim": D, "global_batch": B * world,
+                   "parallelism": f"(b,h) units sharded, {world} independent ranks, no collective",
+                   "l2": "inputs (4 x 128 MiB bf16 per rank) exceed the 126 MB L2; no flush"},
+        "tflops": tflops, "tflops_note": "algorithmic 7*B*H*L^2*d per step (FA causal convention)",
+        "executed_tflops": world * exec_flops * K / (total_ms / 1e3) / 1e12,
+        "ms": {"fwd": fwd_ms, "bwd_phase1": p1_ms, "bwd_phase2": p2_ms},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 3 * K,
+        "clocks": clk, "comparator": comparator,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -14,6 +14,7 @@
  *                blocked.py:218  sb_forward_blocked(q, k, v, layout, **kw)
  *   sb_bwd       blocked.py:299  blocked_backward_twophase(cache, d_o, layout,
  *                                row_offset)     -> (d_q, d_k, d_v, n_stored)
+ *   sb_bwd_phase blocked.py:337-357 / :367-386, the two phases of sb_bwd
  *   sb_snapshot_elems  blocked.py:58-60 BlockLayout.n_tiles x d_block (M/N size)
  *   sb_status_string   the ValueError messages of blocked.py:115-119, :155-156,
  *                      :246-247, :315-316, :398-399
@@ -74,6 +75,14 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
 int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
            const float* row_offset, const float* log_rem, const int32_t* first_kb,
            const float* M, float* N, void* dq, void* dk, void* dv, void* stream);
+
+/* The two kernels of sb_bwd, separately: phases = 1 runs phase 1 (dq and N,
+ * blocked.py:337-357), 2 runs phase 2 (dk, dv from N, blocked.py:367-386),
+ * 3 runs both (== sb_bwd).  Phase 2 must follow phase 1 on the stream. */
+int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void* v,
+                 const void* d_o, const float* row_offset, const float* log_rem,
+                 const int32_t* first_kb, const float* M, float* N, void* dq, void* dk, void* dv,
+                 int phases, void* stream);
 
 const char* sb_status_string(int status);
 int sb_version(void);

@@ -28,8 +28,11 @@ static void FN(sbo_tile_)(const REAL* q, const REAL* k, int d, int rows, int col
                           REAL* z, REAL* lt, REAL* A) {
     for (int r = 0; r < rows; ++r) {
         for (int c = 0; c < cols; ++c) {
+            const REAL* qr = q + (size_t)r * d;
+            const REAL* kc = k + (size_t)c * d;
             REAL s = 0;
-            for (int e = 0; e < d; ++e) s += q[(size_t)r * d + e] * k[(size_t)c * d + e];
+#pragma omp simd reduction(+ : s)
+            for (int e = 0; e < d; ++e) s += qr[e] * kc[e];
             z[r * cols + c] = s * scale;
         }
         for (int c = 0; c < cols; ++c) {
@@ -79,12 +82,15 @@ long long FN(sbo_forward_)(int L, int d, int block, const REAL* q, const REAL* k
             const int ks = kb * block, ke = ks + block < L ? ks + block : L, cols = ke - ks;
             FN(sbo_tile_)(q + (size_t)qs * d, k + (size_t)ks * d, d, rows, cols, kb == qb,
                           scale, a_cur, z, lt, A);
-            for (int r = 0; r < rows; ++r)
+            for (int r = 0; r < rows; ++r) {
+                REAL* orow = o + (size_t)(qs + r) * d;
                 for (int c = 0; c < cols; ++c) {
                     const REAL w = A[r * cols + c];
-                    for (int e = 0; e < d; ++e)
-                        o[(size_t)(qs + r) * d + e] += w * v[(size_t)(ks + c) * d + e];
+                    const REAL* vc = v + (size_t)(ks + c) * d;
+#pragma omp simd
+                    for (int e = 0; e < d; ++e) orow[e] += w * vc[e];
                 }
+            }
             if (M) {
                 REAL* m = M + ((size_t)qb * (qb + 1) / 2 + kb) * block;
                 for (int r = 0; r < rows; ++r) m[r] = a_cur[r];
@@ -112,8 +118,11 @@ static void FN(sbo_dz_)(const REAL* dob, const REAL* vb, int d, int rows, int co
                         REAL* dAt, REAL* dZ) {
     for (int r = 0; r < rows; ++r) {
         for (int c = 0; c < cols; ++c) {
+            const REAL* dr = dob + (size_t)r * d;
+            const REAL* vc = vb + (size_t)c * d;
             REAL s = 0;
-            for (int e = 0; e < d; ++e) s += dob[(size_t)r * d + e] * vb[(size_t)c * d + e];
+#pragma omp simd reduction(+ : s)
+            for (int e = 0; e < d; ++e) s += dr[e] * vc[e];
             if (off) s = s - off[r];
             dAt[r * cols + c] = A[r * cols + c] * s;
         }
@@ -141,6 +150,9 @@ int FN(sbo_backward_twophase_)(int L, int d, int block, const REAL* q, const REA
     REAL *z = (REAL*)malloc(sizeof(REAL) * tb), *lt = (REAL*)malloc(sizeof(REAL) * tb);
     REAL *A = (REAL*)malloc(sizeof(REAL) * tb), *dAt = (REAL*)malloc(sizeof(REAL) * tb);
     REAL *dZ = (REAL*)malloc(sizeof(REAL) * tb), *b = (REAL*)malloc(sizeof(REAL) * block);
+    REAL *acc = (REAL*)malloc(sizeof(REAL) * d);
+    REAL *tk = (REAL*)malloc(sizeof(REAL) * (size_t)block * d);
+    REAL *tv = (REAL*)malloc(sizeof(REAL) * (size_t)block * d);
     memset(dq, 0, sizeof(REAL) * (size_t)L * d);
     memset(dk, 0, sizeof(REAL) * (size_t)L * d);
     memset(dv, 0, sizeof(REAL) * (size_t)L * d);
@@ -160,12 +172,18 @@ int FN(sbo_backward_twophase_)(int L, int d, int block, const REAL* q, const REA
                 for (int c = 0; c < cols; ++c) s += dAt[r * cols + c];
                 b[r] = b[r] + s;
             }
-            for (int r = 0; r < rows; ++r)
-                for (int e = 0; e < d; ++e) {
-                    REAL s = 0;
-                    for (int c = 0; c < cols; ++c) s += dZ[r * cols + c] * k[(size_t)(ks + c) * d + e];
-                    dq[(size_t)(qs + r) * d + e] += s * scale;
+            for (int r = 0; r < rows; ++r) {
+                for (int e = 0; e < d; ++e) acc[e] = 0;
+                for (int c = 0; c < cols; ++c) {
+                    const REAL w = dZ[r * cols + c];
+                    const REAL* kc = k + (size_t)(ks + c) * d;
+#pragma omp simd
+                    for (int e = 0; e < d; ++e) acc[e] += w * kc[e];
                 }
+                REAL* dqr = dq + (size_t)(qs + r) * d;
+#pragma omp simd
+                for (int e = 0; e < d; ++e) dqr[e] += acc[e] * scale;
+            }
         }
     }
     for (int kb = 0; kb < nb; ++kb) {
@@ -178,19 +196,35 @@ int FN(sbo_backward_twophase_)(int L, int d, int block, const REAL* q, const REA
                           scale, M + t * block, z, lt, A);
             FN(sbo_dz_)(d_o + (size_t)qs * d, v + (size_t)ks * d, d, rows, cols,
                         row_offset ? row_offset + qs : NULL, A, lt, N + t * block, dAt, dZ);
-            for (int c = 0; c < cols; ++c)
-                for (int e = 0; e < d; ++e) {
-                    REAL sk = 0, sv = 0;
-                    for (int r = 0; r < rows; ++r) {
-                        sk += dZ[r * cols + c] * q[(size_t)(qs + r) * d + e];
-                        sv += A[r * cols + c] * d_o[(size_t)(qs + r) * d + e];
+            /* dZ^T Q * scale and A^T dO for this tile, rows in ascending order */
+            memset(tk, 0, sizeof(REAL) * (size_t)cols * d);
+            memset(tv, 0, sizeof(REAL) * (size_t)cols * d);
+            for (int r = 0; r < rows; ++r) {
+                const REAL* qr = q + (size_t)(qs + r) * d;
+                const REAL* dr = d_o + (size_t)(qs + r) * d;
+                for (int c = 0; c < cols; ++c) {
+                    const REAL wk = dZ[r * cols + c], wv = A[r * cols + c];
+                    REAL* tkc = tk + (size_t)c * d;
+                    REAL* tvc = tv + (size_t)c * d;
+#pragma omp simd
+                    for (int e = 0; e < d; ++e) {
+                        tkc[e] += wk * qr[e];
+                        tvc[e] += wv * dr[e];
                     }
-                    dk[(size_t)(ks + c) * d + e] += sk * scale;
-                    dv[(size_t)(ks + c) * d + e] += sv;
                 }
+            }
+            for (int c = 0; c < cols; ++c) {
+                REAL* dkc = dk + (size_t)(ks + c) * d;
+                REAL* dvc = dv + (size_t)(ks + c) * d;
+#pragma omp simd
+                for (int e = 0; e < d; ++e) {
+                    dkc[e] += tk[(size_t)c * d + e] * scale;
+                    dvc[e] += tv[(size_t)c * d + e];
+                }
+            }
         }
     }
-    free(z); free(lt); free(A); free(dAt); free(dZ); free(b);
+    free(z); free(lt); free(A); free(dAt); free(dZ); free(b); free(acc); free(tk); free(tv);
     return 0;
 }
 

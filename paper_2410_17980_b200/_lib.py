@@ -27,7 +27,7 @@ class SbParams(ctypes.Structure):
     ]
 
 
-EXPORTS = ("sb_fwd", "sb_bwd", "sb_snapshot_elems", "sb_status_string", "sb_version")
+EXPORTS = ("sb_fwd", "sb_bwd", "sb_bwd_phase", "sb_snapshot_elems", "sb_status_string", "sb_version")
 
 _lib = None
 
@@ -54,6 +54,8 @@ def load(path: str = LIB_PATH):
     lib.sb_fwd.argtypes = [PP, P, P, P, P, P, P, P, P, P]
     lib.sb_bwd.restype = ctypes.c_int
     lib.sb_bwd.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, P, P]
+    lib.sb_bwd_phase.restype = ctypes.c_int
+    lib.sb_bwd_phase.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P]
     lib.sb_status_string.restype = ctypes.c_char_p
     lib.sb_status_string.argtypes = [ctypes.c_int]
     lib.sb_version.restype = ctypes.c_int

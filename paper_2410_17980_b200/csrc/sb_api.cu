@@ -121,6 +121,14 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
 int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
            const float* row_offset, const float* log_rem, const int32_t* first_kb,
            const float* M, float* N, void* dq, void* dk, void* dv, void* stream) {
+  return sb_bwd_phase(p, q, k, v, d_o, row_offset, log_rem, first_kb, M, N, dq, dk, dv, 3, stream);
+}
+
+int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void* v,
+                 const void* d_o, const float* row_offset, const float* log_rem,
+                 const int32_t* first_kb, const float* M, float* N, void* dq, void* dk, void* dv,
+                 int phases, void* stream) {
+  if (phases < 1 || phases > 3) return SB_ERR_SHAPE;
   int st = validate(p);
   if (st) return st;
   (void)log_rem;  // the backward reads the per-tile M snapshots, not the final a
@@ -142,7 +150,8 @@ int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, co
   a.first_kb = first_kb;
   a.M = M;
   a.N = N;
-  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, a, reinterpret_cast<cudaStream_t>(stream));
+  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, a, phases,
+                            reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
 

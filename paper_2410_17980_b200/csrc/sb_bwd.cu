@@ -10,8 +10,6 @@
 //   tiles, b = N snapshot, dK += dZ^T Q, dV += A^T dO — owned rows, no atomics,
 //   deterministic.  dK^T and dV^T are accumulated in TMEM with M = head_dim
 //   (A^T / dZ^T reach the tensor core through MN-major smem descriptors).
-#include <cstdlib>
-
 #include "sb_args.cuh"
 
 namespace sb {
@@ -560,9 +558,7 @@ __global__ void __launch_bounds__(192, 1)
 
 template <int D>
 static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                      const CUtensorMap& tv, const BwdArgs& a, cudaStream_t stream) {
-  const char* dbg = getenv("SB_DEBUG_PHASES");  // "1", "2" or unset (both)
-  const int phases = dbg ? atoi(dbg) : 3;
+                      const CUtensorMap& tv, const BwdArgs& a, int phases, cudaStream_t stream) {
   if (phases & 1) {
     using C = BwdQCfg<D>;
     auto kern = sb_bwd_q_kernel<D>;
@@ -585,9 +581,9 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
 }
 
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                 const CUtensorMap& tv, const BwdArgs& a, cudaStream_t stream) {
-  if (D == 128) return launch_bwd<128>(tq, tdo, tk, tv, a, stream);
-  if (D == 64) return launch_bwd<64>(tq, tdo, tk, tv, a, stream);
+                 const CUtensorMap& tv, const BwdArgs& a, int phases, cudaStream_t stream) {
+  if (D == 128) return launch_bwd<128>(tq, tdo, tk, tv, a, phases, stream);
+  if (D == 64) return launch_bwd<64>(tq, tdo, tk, tv, a, phases, stream);
   return -1;
 }
 

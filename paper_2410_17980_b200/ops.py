@@ -191,7 +191,7 @@ def sb_forward_blocked(q, k, v, layout=None, **kw):
 
 
 def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | None = None,
-                              row_offset=None):
+                              row_offset=None, *, out=None, phases: int = 3):
     """blocked_backward_twophase (blocked.py:299-392) over every (b, h) unit.
 
     Returns (d_q, d_k, d_v, n_stored_tiles).  row_offset (B, H, L) float32 is
@@ -211,16 +211,18 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
         d_o = torch.empty_like(q).copy_(d_o)
     lib = _lib.load()
     p = _params(q, cache.scale, cache.skip, cache.skip_eps)
-    N = torch.empty_like(cache.M)
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    if out is None:  # (N, dq, dk, dv); callers running the phases one by one pass it
+        out = (torch.empty_like(cache.M), torch.empty_like(q), torch.empty_like(q),
+               torch.empty_like(q))
+    N, dq, dk, dv = out
     ro = None
     if row_offset is not None:
         ro = row_offset.to(device=q.device, dtype=torch.float32).contiguous()
         if ro.shape != cache.log_rem.shape:
             raise ValueError("row_offset must be (batch, heads, seq_len)")
-    _lib.check(lib.sb_bwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
-                          _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M), _ptr(N),
-                          _ptr(dq), _ptr(dk), _ptr(dv), _stream()))
+    _lib.check(lib.sb_bwd_phase(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
+                                _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M),
+                                _ptr(N), _ptr(dq), _ptr(dk), _ptr(dv), int(phases), _stream()))
     return dq, dk, dv, cache.layout.n_tiles * q.shape[0] * q.shape[1]
 
 
