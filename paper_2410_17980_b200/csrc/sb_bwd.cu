@@ -10,60 +10,95 @@
 //   tiles, b = N snapshot, dK += dZ^T Q, dV += A^T dO — owned rows, no atomics,
 //   deterministic.  dK^T and dV^T are accumulated in TMEM with M = head_dim
 //   (A^T / dZ^T reach the tensor core through MN-major smem descriptors).
+//
+// Stick warps are split like the forward's: warp w owns rows 32*(w%4)..+31 and
+// key columns [16*(w/4), +16) of the 64-column tile; per row, the four column
+// groups exchange (1) their suffix totals of lt (A needs everything to its
+// right) and (2) their prefix totals of dAt (dZ needs everything to its left)
+// through shared memory, one named barrier each.
 #include "sb_args.cuh"
 
 namespace sb {
 
-// ----------------------------------------------------------------------------
-// Per-row tile recompute shared by both phases. On entry s[] holds the raw
-// q.k dot products of this row (64 key columns); on exit s[] holds A and sg[]
-// holds sigma(z) = 1 - exp(lt) (0 where masked). Ma = M snapshot (log2 units).
-__device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float Ma,
-                                              int lim) {
+constexpr int kBwdGroups = 4;
+constexpr int kBwdCG = kBlock / kBwdGroups;  // 16 key columns per stick thread
+constexpr int kBwdStick = 128 * kBwdGroups;  // 512 stick threads
+constexpr int kBwdThreads = kBwdStick + 64;  // + TMA producer warp + MMA warp
+
+// Per-row, per-tile stick math shared by both phases.
+struct RowTile {
+  float z[kBwdCG];   // Z = z*log2(e), later dAt
+  float cl[kBwdCG];  // local suffix sums of lt, later local prefix sums of dAt
+  float sg[kBwdCG];  // sigma(z) = 1 - exp(lt), 0 where masked
+  float w[kBwdCG];   // dW = dO.V^T
+};
+
+// pass 1: softplus, sigma and the in-group inclusive suffix sums of lt; returns the group total.
+__device__ __forceinline__ float bwd_pass1(RowTile& t, float scale_log2, int c0, int lim) {
   float cum = 0.0f;
 #pragma unroll
-  for (int c = kBlock - 1; c >= 0; --c) {
-    const float Z = s[c] * scale_log2;
-    const float t = ex2(Z);
-    const bool on = c < lim;
-    cum += on ? -softplus2(Z, t) : 0.0f;
-    s[c] = on ? ex2(Z + cum + Ma) : 0.0f;
-    // sigma = t/(1+t); fminf drops the NaN of inf*0 when t overflows (sigma -> 1)
-    sg[c] = on ? fminf(t * rcp(1.0f + t), 1.0f) : 0.0f;
+  for (int c = kBwdCG - 1; c >= 0; --c) {
+    const float Z = t.z[c] * scale_log2;
+    const float e = ex2(Z);
+    const bool on = c0 + c < lim;
+    cum += on ? -softplus2(Z, e) : 0.0f;
+    t.z[c] = Z;
+    t.cl[c] = cum;
+    // sigma = e/(1+e); fminf drops the NaN of inf*0 when e overflows (sigma -> 1)
+    t.sg[c] = on ? fminf(e * rcp(1.0f + e), 1.0f) : 0.0f;
   }
+  return cum;
 }
 
-// dAt = A * (dW - off), dW streamed from TMEM in 16-column chunks.
-__device__ __forceinline__ void load_dat(float* s, uint32_t taddr, float off) {
-#pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    float w[16];
-    tmem_ld16(taddr + ch * 16, w);
-    tmem_wait_ld();
-#pragma unroll
-    for (int c = 0; c < 16; ++c) s[ch * 16 + c] *= (w[c] - off);
-  }
-}
-
-// dZ = dAt - sigma*(prefix(dAt) + b), packed to bf16; returns rowsum(dAt).
-__device__ __forceinline__ float dz_row(const float* dat, const float* sg, float b, uint32_t* pk) {
+// pass 2: A = exp(z + suffix(lt) + M) (base = right groups' lt total + M), dAt = A*(dW - off),
+// in-group inclusive prefix sums of dAt; A packed to bf16 into pa (may be null).
+__device__ __forceinline__ float bwd_pass2(RowTile& t, float base, float off, int c0, int lim,
+                                           uint32_t* pa) {
   float pfx = 0.0f;
 #pragma unroll
-  for (int c = 0; c < kBlock; c += 2) {
-    pfx += dat[c];
-    const float z0 = dat[c] - sg[c] * (pfx + b);
-    pfx += dat[c + 1];
-    const float z1 = dat[c + 1] - sg[c + 1] * (pfx + b);
-    pk[c >> 1] = pack_bf16(z0, z1);
+  for (int c = 0; c < kBwdCG; c += 2) {
+    const float A0 = (c0 + c < lim) ? ex2(t.z[c] + t.cl[c] + base) : 0.0f;
+    const float A1 = (c0 + c + 1 < lim) ? ex2(t.z[c + 1] + t.cl[c + 1] + base) : 0.0f;
+    if (pa) pa[c >> 1] = pack_bf16(A0, A1);
+    t.z[c] = A0 * (t.w[c] - off);
+    t.z[c + 1] = A1 * (t.w[c + 1] - off);
+    pfx += t.z[c];
+    t.cl[c] = pfx;
+    pfx += t.z[c + 1];
+    t.cl[c + 1] = pfx;
   }
   return pfx;
 }
 
-__device__ __forceinline__ void store_row_sw128(uint32_t row_addr, int r, const uint32_t* pk) {
+// pass 3: dZ = dAt - sigma*(prefix(dAt) + b), b = left groups' dAt total + b in effect.
+__device__ __forceinline__ void bwd_pass3(const RowTile& t, float b, uint32_t* pz) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-    st_shared_v4(row_addr + ((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+  for (int c = 0; c < kBwdCG; c += 2)
+    pz[c >> 1] = pack_bf16(t.z[c] - t.sg[c] * (t.cl[c] + b),
+                           t.z[c + 1] - t.sg[c + 1] * (t.cl[c + 1] + b));
+}
+
+// 16 columns (two 16-byte chunks) of one row of a 128B-swizzled K-major tile
+__device__ __forceinline__ void store_cols_sw128(uint32_t row_addr, int r, int gi,
+                                                 const uint32_t* pk) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int chunk = gi * 2 + c;
+    st_shared_v4(row_addr + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
                  pk[4 * c + 3]);
+  }
+}
+
+__device__ __forceinline__ void exchange_sums(const float* xch, int par, int gi, int r,
+                                              float& right, float& left, float& tot) {
+  right = left = tot = 0.0f;
+#pragma unroll
+  for (int g2 = 0; g2 < kBwdGroups; ++g2) {
+    const float v = xch[(par * kBwdGroups + g2) * 128 + r];
+    tot += v;
+    if (g2 > gi) right += v;
+    if (g2 < gi) left += v;
+  }
 }
 
 // ============================================================================
@@ -79,7 +114,8 @@ struct BwdQCfg {
   static constexpr int kOffK = kOffDO + kQBytes;
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kStages * kKVBytes;
-  static constexpr int kOffBar = kOffZ + 2 * kZBytes;
+  static constexpr int kOffX = kOffZ + 2 * kZBytes;  // 2 x [2][NG][128] f32
+  static constexpr int kOffBar = kOffX + 2 * 2 * kBwdGroups * 128 * 4;
   static constexpr int kNumBars = 1 + 3 * kStages + 2 * 4 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
@@ -88,12 +124,13 @@ struct BwdQCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     sb_bwd_q_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                     const BwdArgs args) {
   using C = BwdQCfg<D>;
   constexpr int ST = C::kStages;
+  constexpr int kProdWarp = 4 * kBwdGroups, kMmaWarp = kProdWarp + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -124,6 +161,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bar_zempty = bar_zfull + 2;
   uint64_t* bar_done = bar_zempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+  float* xch1 = reinterpret_cast<float*>(smem + C::kOffX);
+  float* xch2 = xch1 + 2 * kBwdGroups * 128;
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qdo, 1);
@@ -134,20 +173,20 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_sfull + s, 1);
-      mbar_init(bar_sempty + s, 128);
-      mbar_init(bar_zfull + s, 128);
+      mbar_init(bar_sempty + s, kBwdStick);
+      mbar_init(bar_zfull + s, kBwdStick);
       mbar_init(bar_zempty + s, 1);
     }
     mbar_init(bar_done, 1);
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == kProdWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == kProdWarp) {
     if (lane == 0) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_do);
@@ -173,7 +212,7 @@ __global__ void __launch_bounds__(192, 1)
                       c * 64, kb * kBlock, h, b);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T, dO V^T
       constexpr uint32_t idesc_q = idesc_bf16(128, D, 0, 1);   // dZ K: K is MN-major
@@ -223,14 +262,16 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(bar_done);
     }
   } else {
-    const int r = threadIdx.x;
+    const int quarter = warp & 3, gi = warp >> 2;
+    const int r = quarter * 32 + lane;
     const int half = r >> 6;
     const int my_qb = qb0 + half;
     const int row = qt * kTileM + r;
     const bool row_valid = row < g.L;
     const bool half_exists = my_qb < g.nb;
     const int my_first = half ? f1 : f0;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int c0 = gi * kBwdCG;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const float off = (args.row_offset && row_valid) ? args.row_offset[unit * g.L + row] : 0.0f;
     const float* Mrow = args.M + unit * g.n_tiles * kBlock + (r & 63);
     float* Nrow = args.N + unit * g.n_tiles * kBlock + (r & 63);
@@ -239,63 +280,69 @@ __global__ void __launch_bounds__(192, 1)
 
     for (int j = 0; j < n; ++j) {
       const int kb = kb_lo + j;
+      const int par = j & 1;
       const bool live = half_exists && row_valid && kb >= my_first && kb <= my_qb;
-      mbar_wait(bar_sfull + (j & 1), (j >> 1) & 1);
-      tc_fence_after();
-      float s[64], sg[64];
-      uint32_t pk[32];
-      tmem_ld32(tbase + lane_base + C::kColS + (j & 1) * 64, s);
-      tmem_ld32(tbase + lane_base + C::kColS + (j & 1) * 64 + 32, s + 32);
-      tmem_wait_ld();
+      const int lim = (kb == my_qb) ? (r & 63) : kBlock;
       const int64_t t = tile_index(my_qb, kb) * kBlock;
-      if (live) {
-        recompute_row(s, sg, g.scale_log2, Mrow[t], kb == my_qb ? (r & 63) : kBlock);
-      } else {
-#pragma unroll
-        for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
-      }
-      // tcgen05.ld is warp-collective (.sync.aligned): every lane loads dW,
-      // rows outside the sweep just multiply it by A = 0
-      load_dat(s, tbase + lane_base + C::kColW + (j & 1) * 64, off);
+      const float Ma = live ? Mrow[t] : 0.0f;
+      mbar_wait(bar_sfull + par, (j >> 1) & 1);
+      tc_fence_after();
+      RowTile rt;
+      tmem_ld16(tbase + lane_base + C::kColS + par * 64 + c0, rt.z);
+      tmem_ld16(tbase + lane_base + C::kColW + par * 64 + c0, rt.w);
+      tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(bar_sempty + (j & 1));
+      mbar_arrive(bar_sempty + par);
+
+      float part = 0.0f, right, left, tot;
+      if (live) part = bwd_pass1(rt, g.scale_log2, c0, lim);
+      xch1[(par * kBwdGroups + gi) * 128 + r] = part;
+      named_bar_sync(1, kBwdStick);
+      exchange_sums(xch1, par, gi, r, right, left, tot);
+      part = live ? bwd_pass2(rt, right + Ma, off, c0, lim, nullptr) : 0.0f;
+      xch2[(par * kBwdGroups + gi) * 128 + r] = part;
+      named_bar_sync(1, kBwdStick);
+      exchange_sums(xch2, par, gi, r, right, left, tot);
+      uint32_t pz[kBwdCG / 2];
       if (live) {
-        Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
-        bsum += dz_row(s, sg, bsum, pk);
+        bwd_pass3(rt, left + bsum, pz);
+        if (gi == 0) Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
+        bsum += tot;
       } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = 0u;
+        for (int c = 0; c < kBwdCG / 2; ++c) pz[c] = 0u;
       }
-      if (j >= 2) mbar_wait(bar_zempty + (j & 1), ((j >> 1) + 1) & 1);
-      store_row_sw128(z_row + (j & 1) * C::kZBytes, r, pk);
+      if (j >= 2) mbar_wait(bar_zempty + par, ((j >> 1) + 1) & 1);
+      store_cols_sw128(z_row + par * C::kZBytes, r, gi, pz);
       fence_proxy_async_smem();
-      mbar_arrive(bar_zfull + (j & 1));
+      mbar_arrive(bar_zfull + par);
     }
 
     mbar_wait(bar_done, 0);
     tc_fence_after();
+    constexpr int DC = D / kBwdGroups;
     const float scale = g.scale_log2 * kLn2;
-    __nv_bfloat16* dqrow =
-        args.dq + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl;
+    float v[DC];
+    if constexpr (DC == 16) {
+      tmem_ld16(tbase + lane_base + C::kColQ + gi * DC, v);
+    } else {
+      tmem_ld32(tbase + lane_base + C::kColQ + gi * DC, v);
+    }
+    tmem_wait_ld();
+    if (row_valid) {
+      uint4* dst = reinterpret_cast<uint4*>(args.dq + (int64_t)b * g.sb + (int64_t)h * g.sh +
+                                            (int64_t)row * g.sl + gi * DC);
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float v[32];
-      tmem_ld32(tbase + lane_base + C::kColQ + c * 32, v);
-      tmem_wait_ld();
-      if (row_valid) {
-        uint4* dst = reinterpret_cast<uint4*>(dqrow + c * 32);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          dst[q4] = make_uint4(pack_bf16(v[8 * q4] * scale, v[8 * q4 + 1] * scale),
-                               pack_bf16(v[8 * q4 + 2] * scale, v[8 * q4 + 3] * scale),
-                               pack_bf16(v[8 * q4 + 4] * scale, v[8 * q4 + 5] * scale),
-                               pack_bf16(v[8 * q4 + 6] * scale, v[8 * q4 + 7] * scale));
-      }
+      for (int q4 = 0; q4 < DC / 8; ++q4)
+        dst[q4] = make_uint4(pack_bf16(v[8 * q4] * scale, v[8 * q4 + 1] * scale),
+                             pack_bf16(v[8 * q4 + 2] * scale, v[8 * q4 + 3] * scale),
+                             pack_bf16(v[8 * q4 + 4] * scale, v[8 * q4 + 5] * scale),
+                             pack_bf16(v[8 * q4 + 6] * scale, v[8 * q4 + 7] * scale));
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) tmem_dealloc<C::kTmemCols>(tbase);
+  if (warp == kProdWarp) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
 // ============================================================================
@@ -309,10 +356,11 @@ struct BwdKVCfg {
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kKVBytes;
   static constexpr int kOffQ = kOffV + kKVBytes;                  // stage s: Q at +s*2*kQBytes
-  static constexpr int kOffA = kOffQ + kStages * 2 * kQBytes;     // A[2]
-  static constexpr int kOffZ = kOffA + 2 * kPBytes;               // dZ[2]
-  static constexpr int kOffBar = kOffZ + 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 * 6 + 1;
+  static constexpr int kOffA = kOffQ + kStages * 2 * kQBytes;     // A (single buffer)
+  static constexpr int kOffZ = kOffA + kPBytes;                   // dZ (single buffer)
+  static constexpr int kOffX = kOffZ + kPBytes;
+  static constexpr int kOffBar = kOffX + 2 * 2 * kBwdGroups * 128 * 4;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 4 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;
@@ -331,12 +379,13 @@ __device__ __forceinline__ int next_live_qt(const int* fkb, int nb, int n_qt, in
 }
 
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     sb_bwd_kv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                      const BwdArgs args) {
   using C = BwdKVCfg<D>;
   constexpr int ST = C::kStages;
+  constexpr int kProdWarp = 4 * kBwdGroups, kMmaWarp = kProdWarp + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -357,11 +406,13 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bar_sfull = bar_qempty + ST;
   uint64_t* bar_sempty = bar_sfull + 2;
   uint64_t* bar_afull = bar_sempty + 2;
-  uint64_t* bar_aempty = bar_afull + 2;
-  uint64_t* bar_zfull = bar_aempty + 2;
-  uint64_t* bar_zempty = bar_zfull + 2;
-  uint64_t* bar_done = bar_zempty + 2;
+  uint64_t* bar_aempty = bar_afull + 1;
+  uint64_t* bar_zfull = bar_aempty + 1;
+  uint64_t* bar_zempty = bar_zfull + 1;
+  uint64_t* bar_done = bar_zempty + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+  float* xch1 = reinterpret_cast<float*>(smem + C::kOffX);
+  float* xch2 = xch1 + 2 * kBwdGroups * 128;
 
   if (threadIdx.x == 0) {
     mbar_init(bar_kv, 1);
@@ -371,23 +422,23 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_sfull + s, 1);
-      mbar_init(bar_sempty + s, 128);
-      mbar_init(bar_afull + s, 128);
-      mbar_init(bar_aempty + s, 1);
-      mbar_init(bar_zfull + s, 128);
-      mbar_init(bar_zempty + s, 1);
+      mbar_init(bar_sempty + s, kBwdStick);
     }
+    mbar_init(bar_afull, kBwdStick);
+    mbar_init(bar_aempty, 1);
+    mbar_init(bar_zfull, kBwdStick);
+    mbar_init(bar_zempty, 1);
     mbar_init(bar_done, 1);
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == kProdWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const bool any = qt_first < g.n_qt;
 
-  if (warp == 4) {
+  if (warp == kProdWarp) {
     if (lane == 0 && any) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_do);
@@ -411,7 +462,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0 && any) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T, dO V^T
       constexpr uint32_t idesc_t = idesc_bf16(D, 64, 1, 1);    // dO^T A, Q^T dZ: both MN-major
@@ -424,22 +475,20 @@ __global__ void __launch_bounds__(192, 1)
       auto issue_kv = [&](int i) {
         const int s = i % ST;
         const uint32_t qa = q0_addr + s * 2 * C::kQBytes, da = qa + C::kQBytes;
-        mbar_wait(bar_afull + (i & 1), (i >> 1) & 1);
+        mbar_wait(bar_afull, i & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kTileM / 16; ++k)  // dV^T += dO^T A  (K = query rows)
           umma_ss(tbase + C::kColV, sdesc_sw128(da + k * 2048, kTileM * 128, 1024),
-                  sdesc_sw128(a_addr + (i & 1) * C::kPBytes + k * 2048, 16, 1024), idesc_t,
-                  (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(bar_aempty + (i & 1));
-        mbar_wait(bar_zfull + (i & 1), (i >> 1) & 1);
+                  sdesc_sw128(a_addr + k * 2048, 16, 1024), idesc_t, (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(bar_aempty);
+        mbar_wait(bar_zfull, i & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kTileM / 16; ++k)  // dK^T += Q^T dZ
           umma_ss(tbase + C::kColK, sdesc_sw128(qa + k * 2048, kTileM * 128, 1024),
-                  sdesc_sw128(z_addr + (i & 1) * C::kPBytes + k * 2048, 16, 1024), idesc_t,
-                  (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(bar_zempty + (i & 1));
+                  sdesc_sw128(z_addr + k * 2048, 16, 1024), idesc_t, (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(bar_zempty);
         umma_commit(bar_qempty + s);
       };
       int j = 0;
@@ -470,90 +519,101 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(bar_done);
     }
   } else {
-    const int r = threadIdx.x;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int quarter = warp & 3, gi = warp >> 2;
+    const int r = quarter * 32 + lane;
+    const int c0 = gi * kBwdCG;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const float* Mbase = args.M + unit * g.n_tiles * kBlock + (r & 63);
     const float* Nbase = args.N + unit * g.n_tiles * kBlock + (r & 63);
     const uint32_t a_row = smem_u32(smem + C::kOffA) + r * 128;
     const uint32_t z_row = smem_u32(smem + C::kOffZ) + r * 128;
     int j = 0;
     for (int qt = qt_first; qt < g.n_qt; qt = next_live_qt(fkb, g.nb, g.n_qt, kb, qt + 1), ++j) {
+      const int par = j & 1;
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
       const bool live = row < g.L && my_qb >= kb && fkb[my_qb] <= kb;
-      mbar_wait(bar_sfull + (j & 1), (j >> 1) & 1);
-      tc_fence_after();
-      float s[64], sg[64];
-      uint32_t pa[32], pz[32];
-      tmem_ld32(tbase + lane_base + C::kColS + (j & 1) * 64, s);
-      tmem_ld32(tbase + lane_base + C::kColS + (j & 1) * 64 + 32, s + 32);
-      tmem_wait_ld();
+      const int lim = (kb == my_qb) ? (r & 63) : kBlock;
       const int64_t t = tile_index(my_qb, kb) * kBlock;
-      float off = 0.0f;
+      float Ma = 0.0f, Nb = 0.0f, off = 0.0f;
       if (live) {
+        Ma = Mbase[t];
+        Nb = Nbase[t];
         off = args.row_offset ? args.row_offset[unit * g.L + row] : 0.0f;
-        recompute_row(s, sg, g.scale_log2, Mbase[t], kb == my_qb ? (r & 63) : kBlock);
-      } else {
-#pragma unroll
-        for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
       }
-#pragma unroll
-      for (int c = 0; c < 32; ++c) pa[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
-      load_dat(s, tbase + lane_base + C::kColW + (j & 1) * 64, off);  // warp-collective
+      mbar_wait(bar_sfull + par, (j >> 1) & 1);
+      tc_fence_after();
+      RowTile rt;
+      tmem_ld16(tbase + lane_base + C::kColS + par * 64 + c0, rt.z);
+      tmem_ld16(tbase + lane_base + C::kColW + par * 64 + c0, rt.w);
+      tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(bar_sempty + (j & 1));
+      mbar_arrive(bar_sempty + par);
+
+      float part = 0.0f, right, left, tot;
+      if (live) part = bwd_pass1(rt, g.scale_log2, c0, lim);
+      xch1[(par * kBwdGroups + gi) * 128 + r] = part;
+      named_bar_sync(1, kBwdStick);
+      exchange_sums(xch1, par, gi, r, right, left, tot);
+      uint32_t pa[kBwdCG / 2], pz[kBwdCG / 2];
       if (live) {
-        dz_row(s, sg, Nbase[t], pz);
+        part = bwd_pass2(rt, right + Ma, off, c0, lim, pa);
+      } else {
+        part = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kBwdCG / 2; ++c) pa[c] = 0u;
+      }
+      if (j >= 1) mbar_wait(bar_aempty, (j - 1) & 1);
+      store_cols_sw128(a_row, r, gi, pa);
+      fence_proxy_async_smem();
+      mbar_arrive(bar_afull);
+      xch2[(par * kBwdGroups + gi) * 128 + r] = part;
+      named_bar_sync(1, kBwdStick);
+      exchange_sums(xch2, par, gi, r, right, left, tot);
+      if (live) {
+        bwd_pass3(rt, left + Nb, pz);
       } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) pz[c] = 0u;
+        for (int c = 0; c < kBwdCG / 2; ++c) pz[c] = 0u;
       }
-      if (j >= 2) mbar_wait(bar_aempty + (j & 1), ((j >> 1) + 1) & 1);
-      store_row_sw128(a_row + (j & 1) * C::kPBytes, r, pa);
+      if (j >= 1) mbar_wait(bar_zempty, (j - 1) & 1);
+      store_cols_sw128(z_row, r, gi, pz);
       fence_proxy_async_smem();
-      mbar_arrive(bar_afull + (j & 1));
-      if (j >= 2) mbar_wait(bar_zempty + (j & 1), ((j >> 1) + 1) & 1);
-      store_row_sw128(z_row + (j & 1) * C::kPBytes, r, pz);
-      fence_proxy_async_smem();
-      mbar_arrive(bar_zfull + (j & 1));
+      mbar_arrive(bar_zfull);
     }
 
-    // epilogue: TMEM holds dV^T / dK^T (lanes = head-dim index, columns = keys).
+    // epilogue: TMEM holds dV^T / dK^T (lanes = head-dim index, columns = keys);
+    // column group gi owns keys [16*gi, 16*gi+16).
     // M = 128: lane r <-> d = r.  M = 64: rows 16w+i live in lanes 32w+i, i < 16.
-    const int dlane = (D == 128) ? r : ((r & 31) < 16 ? (warp * 16 + (r & 15)) : -1);
+    const int dlane = (D == 128) ? r : (lane < 16 ? (quarter * 16 + lane) : -1);
+    float vv[kBwdCG], kk[kBwdCG];
     if (any) {
       mbar_wait(bar_done, 0);
       tc_fence_after();
+      tmem_ld16(tbase + lane_base + C::kColV + c0, vv);
+      tmem_ld16(tbase + lane_base + C::kColK + c0, kk);
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int c = 0; c < kBwdCG; ++c) vv[c] = kk[c] = 0.0f;
     }
     const float scale = g.scale_log2 * kLn2;
     const int64_t base = (int64_t)b * g.sb + (int64_t)h * g.sh;
+    if (dlane >= 0) {
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      float vv[32], kk[32];
-      if (any) {
-        tmem_ld32(tbase + lane_base + C::kColV + half * 32, vv);
-        tmem_ld32(tbase + lane_base + C::kColK + half * 32, kk);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) vv[c] = kk[c] = 0.0f;
-      }
-      if (dlane >= 0) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int key = kb * kBlock + half * 32 + c;
-          if (key < g.L) {
-            const int64_t o = base + (int64_t)key * g.sl + dlane;
-            args.dv[o] = __float2bfloat16_rn(vv[c]);
-            args.dk[o] = __float2bfloat16_rn(kk[c] * scale);
-          }
+      for (int c = 0; c < kBwdCG; ++c) {
+        const int key = kb * kBlock + c0 + c;
+        if (key < g.L) {
+          const int64_t o = base + (int64_t)key * g.sl + dlane;
+          args.dv[o] = __float2bfloat16_rn(vv[c]);
+          args.dk[o] = __float2bfloat16_rn(kk[c] * scale);
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) tmem_dealloc<C::kTmemCols>(tbase);
+  if (warp == kProdWarp) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
 template <int D>
@@ -565,7 +625,8 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
-    kern<<<(unsigned)(a.g.n_qt * a.g.B * a.g.H), 192, C::kSmem, stream>>>(tq, tdo, tk, tv, a);
+    kern<<<(unsigned)(a.g.n_qt * a.g.B * a.g.H), kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk,
+                                                                                   tv, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   }
   if (phases & 2) {
@@ -574,7 +635,8 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
-    kern<<<(unsigned)(a.g.nb * a.g.B * a.g.H), 192, C::kSmem, stream>>>(tq, tdo, tk, tv, a);
+    kern<<<(unsigned)(a.g.nb * a.g.B * a.g.H), kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tv,
+                                                                                 a);
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   }
   return 0;

@@ -10,22 +10,27 @@
 //
 // One CTA = one (b, h, 128-row query tile) = two reference query blocks
 // (64-row skip groups). Warp roles:
-//   warps 0-3  "stick" warps: thread r owns query row r. tcgen05.ld the S tile
-//              row from TMEM, run the sequential right-to-left suffix scan in
-//              registers (same order as np.cumsum), write A (bf16) into a
-//              128B-swizzled smem tile for the A*V MMA; epilogue O, a.
-//   warp 4     TMEM allocator + TMA producer (lane 0): Q once, K/V ring.
-//   warp 5     MMA issuer (lane 0): S = Q K^T (TMEM, double buffered),
+//   warps 0..4*NG-1  "stick" warps. Warp w owns TMEM lanes (= query rows)
+//              32*(w%4)..+31 and key columns [CG*(w/4), CG*(w/4)+CG) of every
+//              64-column S tile (CG = 64/NG). Each thread scans its CG columns
+//              right to left in registers; the NG column groups of a row combine
+//              their partial suffix sums of lt through shared memory (one named
+//              barrier per tile), then write A (bf16) into the 128B-swizzled
+//              smem tile read by the A*V MMA.
+//   warp 4*NG   TMEM allocator + TMA producer (lane 0): Q once, K/V ring.
+//   warp 4*NG+1 MMA issuer (lane 0): S = Q K^T (TMEM, double buffered),
 //              O += A V (TMEM accumulator, no rescaling — stick-breaking
 //              weights are absolute).
 #include "sb_args.cuh"
 
 namespace sb {
 
-
-template <int D>
+template <int D, int NG>
 struct FwdCfg {
   static constexpr int kStages = D == 128 ? 3 : 4;
+  static constexpr int kCG = kBlock / NG;             // key columns per group
+  static constexpr int kStick = 128 * NG;             // stick threads
+  static constexpr int kThreads = kStick + 64;
   static constexpr int kQBytes = kTileM * D * 2;      // 128 x D bf16
   static constexpr int kKVBytes = kBlock * D * 2;     // 64 x D bf16
   static constexpr int kPBytes = kTileM * kBlock * 2; // 128 x 64 bf16
@@ -33,20 +38,24 @@ struct FwdCfg {
   static constexpr int kOffK = kOffQ + kQBytes;
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffP = kOffV + kStages * kKVBytes;
-  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  static constexpr int kOffX = kOffP + 2 * kPBytes;         // [2][NG][128] f32 partial sums
+  static constexpr int kOffRed = kOffX + 2 * NG * 128 * 4;  // [2][4] f64 per-warp max(a)
+  static constexpr int kOffBar = kOffRed + 2 * 4 * 8;
   static constexpr int kNumBars = 1 + 3 * kStages + 2 + 2 + 2 + 2 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
-  static constexpr int kSmem = kOffMisc + 128 + 1024;  // + alignment slack
+  static constexpr int kSmem = kOffMisc + 64 + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = 256;           // S[2] (2x64) + O (D <= 128)
   static constexpr uint32_t kColS = 0, kColO = 128;
 };
 
-template <int D, bool kSkip>
-__global__ void __launch_bounds__(192, 1)
+template <int D, int NG, bool kSkip>
+__global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
     sb_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const FwdArgs args) {
-  using C = FwdCfg<D>;
+  using C = FwdCfg<D, NG>;
   constexpr int ST = C::kStages;
+  constexpr int CG = C::kCG;
+  constexpr int kProdWarp = 4 * NG, kMmaWarp = 4 * NG + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -73,9 +82,10 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bar_pempty = bar_pfull + 2;
   uint64_t* bar_ofull = bar_pempty + 2;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
-  uint32_t* tmem_slot = misc;                        // TMEM base address
-  volatile int* n_eff = reinterpret_cast<volatile int*>(misc + 1);  // tiles to run
-  double* red = reinterpret_cast<double*>(misc + 2); // [2][4] per-warp max(a) (skip)
+  uint32_t* tmem_slot = misc;                                       // TMEM base address
+  volatile int* n_eff = reinterpret_cast<volatile int*>(misc + 1);  // tiles the MMA consumes
+  float* xch = reinterpret_cast<float*>(smem + C::kOffX);
+  double* red = reinterpret_cast<double*>(smem + C::kOffRed);
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
@@ -86,21 +96,21 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_sfull + s, 1);
-      mbar_init(bar_sempty + s, 128);
-      mbar_init(bar_pfull + s, 128);
+      mbar_init(bar_sempty + s, C::kStick);
+      mbar_init(bar_pfull + s, C::kStick);
       mbar_init(bar_pempty + s, 1);
     }
     mbar_init(bar_ofull, 1);
     *n_eff = n_kv;
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == kProdWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == kProdWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       tma_prefetch(&tm_q);
@@ -139,7 +149,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(bar_vfull + (j % ST), (j / ST) & 1);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T: both K-major
@@ -196,140 +206,162 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ------------------------------------------------------------ stick warps
-    const int r = threadIdx.x;  // 0..127 == TMEM lane == query row in the tile
+    const int quarter = warp & 3, gi = warp >> 2;  // row quarter, column group
+    const int r = quarter * 32 + lane;             // TMEM lane == query row in the tile
     const int half = r >> 6;
     const int my_qb = qb0 + half;
     const int row = qt * kTileM + r;
     const bool row_valid = row < g.L;
-    const bool half_exists = my_qb < g.nb;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int64_t unit = (int64_t)b * g.H + h;
     float* Mrow = args.M ? args.M + unit * g.n_tiles * kBlock + (r & 63) : nullptr;
-    uint8_t* pbuf = smem + C::kOffP;
-    const uint32_t p_row = smem_u32(pbuf) + r * 128;
+    const uint32_t p_row = smem_u32(smem + C::kOffP) + r * 128;
+    const int c0 = gi * CG;  // first key column of this group
 
     double a_d = 0.0;      // running log remaining mass (natural log), f64
     float a2 = 0.0f;       // same in log2 units, f32, feeds the exponent
-    bool act[2] = {qb0 < g.nb, qb0 + 1 < g.nb};  // halves still sweeping (skip)
-    bool active = half_exists;  // this row's half has not hit the skip criterion
-    int lowest = my_qb;         // leftmost processed key block (first_kb)
+    bool act[2] = {qb0 < g.nb, qb0 + 1 < g.nb};  // halves still sweeping
+    int lowest = my_qb;    // leftmost processed key block (first_kb)
     int visited = 0;
-    int j = 0;
-    for (; j < n_kv; ++j) {
+    for (int j = 0; j < n_kv; ++j) {
       const int kb = kb_hi - j;
-      mbar_wait(bar_sfull + (j & 1), (j >> 1) & 1);
+      const int par = j & 1;
+      mbar_wait(bar_sfull + par, (j >> 1) & 1);
       tc_fence_after();
-      float s[64];
-      tmem_ld32(tbase + lane_base + C::kColS + (j & 1) * 64, s);
-      tmem_ld32(tbase + lane_base + C::kColS + (j & 1) * 64 + 32, s + 32);
+      float zs[CG], cl[CG];
+      if constexpr (CG == 16) {
+        tmem_ld16(tbase + lane_base + C::kColS + par * 64 + c0, zs);
+      } else {
+        tmem_ld32(tbase + lane_base + C::kColS + par * 64 + c0, zs);
+      }
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(bar_sempty + (j & 1));
+      mbar_arrive(bar_sempty + par);
 
-      const bool live = active && kb <= my_qb;  // tile belongs to this row's sweep
-      uint32_t pk[32];
-      if (live) {
-        const int lim = (kb == my_qb) ? (r & 63) : kBlock;  // strict causality on the diagonal
-        float cum = 0.0f;
+      // pass 1: softplus and the local (in-group) inclusive suffix sums of lt
+      const bool mine = act[half] && kb <= my_qb;
+      const int lim = (kb == my_qb) ? (r & 63) : kBlock;  // strict causality on the diagonal
+      float cum = 0.0f;
+      if (mine) {
 #pragma unroll
-        for (int c = kBlock - 1; c >= 0; --c) {
-          const float Z = s[c] * g.scale_log2;
-          const float t = ex2(Z);
-          const float lt = (c < lim) ? -softplus2(Z, t) : 0.0f;
-          cum += lt;
-          s[c] = (c < lim) ? ex2(Z + cum + a2) : 0.0f;
+        for (int c = CG - 1; c >= 0; --c) {
+          const float Z = zs[c] * g.scale_log2;
+          const bool on = c0 + c < lim;
+          cum += on ? -softplus2(Z, ex2(Z)) : 0.0f;
+          zs[c] = Z;
+          cl[c] = cum;
         }
+      }
+      xch[(par * NG + gi) * 128 + r] = cum;
+      if (kSkip && gi == 0 && j > 0) {
+        // skip check for this tile (blocked.py:175-176), on a after the previous one
+        double m = row_valid ? a_d : -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
-        if (Mrow && row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
-        a_d += (double)cum * (double)kLn2;
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) red[par * 4 + quarter] = m;
+      }
+      named_bar_sync(1, C::kStick);
+      if (kSkip && j > 0) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const double mh = fmax(red[par * 4 + 2 * hh], red[par * 4 + 2 * hh + 1]);
+          if (act[hh] && kb < qb0 + hh && mh < args.log_eps) act[hh] = false;
+        }
+      }
+      const bool live = act[half] && kb <= my_qb;
+      float right = 0.0f, tot = 0.0f;  // lt sums of the groups right of mine / of the row
+#pragma unroll
+      for (int g2 = 0; g2 < NG; ++g2) {
+        const float v = xch[(par * NG + g2) * 128 + r];
+        tot += v;
+        if (g2 > gi) right += v;
+      }
+      uint32_t pk[CG / 2];
+      if (live) {
+        const float base = right + a2;
+#pragma unroll
+        for (int c = 0; c < CG; c += 2) {
+          const float A0 = (c0 + c < lim) ? ex2(zs[c] + cl[c] + base) : 0.0f;
+          const float A1 = (c0 + c + 1 < lim) ? ex2(zs[c + 1] + cl[c + 1] + base) : 0.0f;
+          pk[c >> 1] = pack_bf16(A0, A1);
+        }
+        if (gi == 0 && Mrow && row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
+        a_d += (double)tot * (double)kLn2;
         a2 = (float)(a_d * 1.4426950408889634);
         lowest = kb;
         ++visited;
       } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = 0u;
+        for (int c = 0; c < CG / 2; ++c) pk[c] = 0u;
       }
-      if (j >= 2) mbar_wait(bar_pempty + (j & 1), ((j >> 1) + 1) & 1);
-      const uint32_t pb = p_row + (j & 1) * C::kPBytes;
+      const bool stop = kSkip && !act[0] && !act[1];
+      if (stop && r == 0 && gi == 0) *n_eff = j + 1;  // tile j (all-zero A) is the last one
+      if (j >= 2) mbar_wait(bar_pempty + par, ((j >> 1) + 1) & 1);
+      const uint32_t pb = p_row + par * C::kPBytes;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        st_shared_v4(pb + ((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+      for (int c = 0; c < CG / 8; ++c) {
+        const int chunk = gi * (CG / 8) + c;
+        st_shared_v4(pb + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
                      pk[4 * c + 3]);
-      fence_proxy_async_smem();
-
-      bool stop = false;
-      if (kSkip) {
-        // decision for the next key block kb-1 (blocked.py:175-176), per 64-row
-        // half: max over its rows of a < log(eps), checked only left of the
-        // half's diagonal. Every stick thread derives both halves' state from
-        // the same per-warp maxima, so the decision is CTA-uniform.
-        double m = row_valid ? a_d : -INFINITY;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) red[(j & 1) * 4 + warp] = m;
-        named_bar_sync(1, 128);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const double mh = fmax(red[(j & 1) * 4 + 2 * hh], red[(j & 1) * 4 + 2 * hh + 1]);
-          if (act[hh] && (kb - 1) < qb0 + hh && mh < args.log_eps) act[hh] = false;
-        }
-        active = act[half];
-        stop = !act[0] && !act[1];
-        if (stop && r == 0) *n_eff = j + 1;
       }
-      mbar_arrive(bar_pfull + (j & 1));
+      fence_proxy_async_smem();
+      mbar_arrive(bar_pfull + par);
       if (stop) break;
     }
 
     // ------------------------------------------------------------ epilogue
     mbar_wait(bar_ofull, 0);
     tc_fence_after();
-    __nv_bfloat16* orow = args.o + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float ov[32];
-      tmem_ld32(tbase + lane_base + C::kColO + c * 32, ov);
-      tmem_wait_ld();
-      if (row_valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          dst[q4] = make_uint4(pack_bf16(ov[8 * q4], ov[8 * q4 + 1]),
-                               pack_bf16(ov[8 * q4 + 2], ov[8 * q4 + 3]),
-                               pack_bf16(ov[8 * q4 + 4], ov[8 * q4 + 5]),
-                               pack_bf16(ov[8 * q4 + 6], ov[8 * q4 + 7]));
-      }
+    constexpr int DC = D / NG;  // output columns per group (16 or 32)
+    float ov[DC];
+    if constexpr (DC == 16) {
+      tmem_ld16(tbase + lane_base + C::kColO + gi * DC, ov);
+    } else {
+      tmem_ld32(tbase + lane_base + C::kColO + gi * DC, ov);
     }
-    if (row_valid) args.log_rem[unit * g.L + row] = (float)a_d;
-    if (half_exists && (r & 63) == 0) {
+    tmem_wait_ld();
+    if (row_valid) {
+      __nv_bfloat16* orow =
+          args.o + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl + gi * DC;
+      uint4* dst = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+      for (int q4 = 0; q4 < DC / 8; ++q4)
+        dst[q4] = make_uint4(pack_bf16(ov[8 * q4], ov[8 * q4 + 1]),
+                             pack_bf16(ov[8 * q4 + 2], ov[8 * q4 + 3]),
+                             pack_bf16(ov[8 * q4 + 4], ov[8 * q4 + 5]),
+                             pack_bf16(ov[8 * q4 + 6], ov[8 * q4 + 7]));
+      if (gi == 0) args.log_rem[unit * g.L + row] = (float)a_d;
+    }
+    if (gi == 0 && my_qb < g.nb && (r & 63) == 0) {
       args.first_kb[unit * g.nb + my_qb] = lowest;
       if (args.counters) atomicAdd(args.counters, (unsigned long long)visited);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) tmem_dealloc<C::kTmemCols>(tbase);
+  if (warp == kProdWarp) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
-template <int D, bool kSkip>
+template <int D, int NG, bool kSkip>
 static int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                       const FwdArgs& a, cudaStream_t stream) {
-  using C = FwdCfg<D>;
-  auto kern = sb_fwd_kernel<D, kSkip>;
+  using C = FwdCfg<D, NG>;
+  auto kern = sb_fwd_kernel<D, NG, kSkip>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return (int)e;
   const unsigned grid = (unsigned)(a.g.n_qt * a.g.B * a.g.H);
-  kern<<<grid, 192, C::kSmem, stream>>>(tq, tk, tv, a);
+  kern<<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, a);
   return (int)cudaGetLastError();
 }
 
+constexpr int kFwdGroups = 4;
+
 int fwd_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
                  const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream) {
-  if (D == 128) return skip ? launch_fwd<128, true>(tq, tk, tv, a, stream)
-                            : launch_fwd<128, false>(tq, tk, tv, a, stream);
-  if (D == 64) return skip ? launch_fwd<64, true>(tq, tk, tv, a, stream)
-                           : launch_fwd<64, false>(tq, tk, tv, a, stream);
+  if (D == 128) return skip ? launch_fwd<128, kFwdGroups, true>(tq, tk, tv, a, stream)
+                            : launch_fwd<128, kFwdGroups, false>(tq, tk, tv, a, stream);
+  if (D == 64) return skip ? launch_fwd<64, kFwdGroups, true>(tq, tk, tv, a, stream)
+                           : launch_fwd<64, kFwdGroups, false>(tq, tk, tv, a, stream);
   return -1;
 }
 
