@@ -25,40 +25,30 @@ constexpr int kBwdCG = kBlock / kBwdGroups;  // 16 key columns per stick thread
 constexpr int kBwdStick = 128 * kBwdGroups;  // 512 stick threads
 constexpr int kBwdThreads = kBwdStick + 64;  // + TMA producer warp + MMA warp
 
-// Per-row, per-tile stick math shared by both phases.
+// Per-row, per-tile stick math shared by both phases (product form, see
+// sb_common.cuh: A_c = sigma_c * prod_{c'>c} r_c' * e^M, sigma = t/(1+t)).
 struct RowTile {
   float z[kBwdCG];   // Z = z*log2(e), later dAt
-  float cl[kBwdCG];  // local suffix sums of lt, later local prefix sums of dAt
+  float cl[kBwdCG];  // sigma_c * in-group suffix product of r, later prefix sums of dAt
   float sg[kBwdCG];  // sigma(z) = 1 - exp(lt), 0 where masked
   float w[kBwdCG];   // dW = dO.V^T
 };
 
-// pass 1: softplus, sigma and the in-group inclusive suffix sums of lt; returns the group total.
+// pass 1: sigma, r and the in-group suffix products; returns the group's product of r.
+template <bool kDiag>
 __device__ __forceinline__ float bwd_pass1(RowTile& t, float scale_log2, int c0, int lim) {
-  float cum = 0.0f;
-#pragma unroll
-  for (int c = kBwdCG - 1; c >= 0; --c) {
-    const float Z = t.z[c] * scale_log2;
-    const float e = ex2(Z);
-    const bool on = c0 + c < lim;
-    cum += on ? -softplus2(Z, e) : 0.0f;
-    t.z[c] = Z;
-    t.cl[c] = cum;
-    // sigma = e/(1+e); fminf drops the NaN of inf*0 when e overflows (sigma -> 1)
-    t.sg[c] = on ? fminf(e * rcp(1.0f + e), 1.0f) : 0.0f;
-  }
-  return cum;
+  return prod_pass<kBwdCG, kDiag>(t.z, t.cl, t.sg, scale_log2, c0, lim);
 }
 
-// pass 2: A = exp(z + suffix(lt) + M) (base = right groups' lt total + M), dAt = A*(dW - off),
-// in-group inclusive prefix sums of dAt; A packed to bf16 into pa (may be null).
-__device__ __forceinline__ float bwd_pass2(RowTile& t, float base, float off, int c0, int lim,
-                                           uint32_t* pa) {
+// pass 2: A = cl*base (base = e^M * product of r right of this group),
+// dAt = A*(dW - off), in-group inclusive prefix sums of dAt; A packed to bf16
+// into pa (may be null). Returns the group's dAt total.
+__device__ __forceinline__ float bwd_pass2(RowTile& t, float base, float off, uint32_t* pa) {
   float pfx = 0.0f;
 #pragma unroll
   for (int c = 0; c < kBwdCG; c += 2) {
-    const float A0 = (c0 + c < lim) ? ex2(t.z[c] + t.cl[c] + base) : 0.0f;
-    const float A1 = (c0 + c + 1 < lim) ? ex2(t.z[c + 1] + t.cl[c + 1] + base) : 0.0f;
+    const float A0 = t.cl[c] * base;
+    const float A1 = t.cl[c + 1] * base;
     if (pa) pa[c >> 1] = pack_bf16(A0, A1);
     t.z[c] = A0 * (t.w[c] - off);
     t.z[c + 1] = A1 * (t.w[c + 1] - off);
@@ -87,6 +77,15 @@ __device__ __forceinline__ void store_cols_sw128(uint32_t row_addr, int r, int g
     st_shared_v4(row_addr + ((chunk ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
                  pk[4 * c + 3]);
   }
+}
+
+// product of the r-products of the groups right of mine
+__device__ __forceinline__ float exchange_right_prod(const float* xch, int par, int gi, int r) {
+  float p = 1.0f;
+#pragma unroll
+  for (int g2 = 0; g2 < kBwdGroups; ++g2)
+    if (g2 > gi) p *= xch[(par * kBwdGroups + g2) * 128 + r];
+  return p;
 }
 
 __device__ __forceinline__ void exchange_sums(const float* xch, int par, int gi, int r,
@@ -294,12 +293,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(bar_sempty + par);
 
-      float part = 0.0f, right, left, tot;
-      if (live) part = bwd_pass1(rt, g.scale_log2, c0, lim);
+      const bool diag = kb == my_qb;  // warp-uniform
+      float part = 1.0f, right, left, tot;
+      if (live)
+        part = diag ? bwd_pass1<true>(rt, g.scale_log2, c0, lim)
+                    : bwd_pass1<false>(rt, g.scale_log2, c0, lim);
       xch1[(par * kBwdGroups + gi) * 128 + r] = part;
       named_bar_sync(1, kBwdStick);
-      exchange_sums(xch1, par, gi, r, right, left, tot);
-      part = live ? bwd_pass2(rt, right + Ma, off, c0, lim, nullptr) : 0.0f;
+      right = exchange_right_prod(xch1, par, gi, r);
+      part = live ? bwd_pass2(rt, ex2(Ma) * right, off, nullptr) : 0.0f;
       xch2[(par * kBwdGroups + gi) * 128 + r] = part;
       named_bar_sync(1, kBwdStick);
       exchange_sums(xch2, par, gi, r, right, left, tot);
@@ -550,14 +552,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(bar_sempty + par);
 
-      float part = 0.0f, right, left, tot;
-      if (live) part = bwd_pass1(rt, g.scale_log2, c0, lim);
+      const bool diag = kb == my_qb;  // warp-uniform
+      float part = 1.0f, right, left, tot;
+      if (live)
+        part = diag ? bwd_pass1<true>(rt, g.scale_log2, c0, lim)
+                    : bwd_pass1<false>(rt, g.scale_log2, c0, lim);
       xch1[(par * kBwdGroups + gi) * 128 + r] = part;
       named_bar_sync(1, kBwdStick);
-      exchange_sums(xch1, par, gi, r, right, left, tot);
+      right = exchange_right_prod(xch1, par, gi, r);
       uint32_t pa[kBwdCG / 2], pz[kBwdCG / 2];
       if (live) {
-        part = bwd_pass2(rt, right + Ma, off, c0, lim, pa);
+        part = bwd_pass2(rt, ex2(Ma) * right, off, pa);
       } else {
         part = 0.0f;
 #pragma unroll

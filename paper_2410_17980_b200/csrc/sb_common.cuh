@@ -47,4 +47,73 @@ __device__ __forceinline__ float softplus2(float Z, float t) {
   return Z > kSoftplusThr2 ? Z : sp;
 }
 
+// Product-form tile math (SURVEY.md §7 "in-tile product form"): with t = e^z and
+// r = 1/(1+t) = exp(lt), sigma = t*r and the suffix product of r replaces the
+// suffix sum of lt, so A_c = sigma_c * prod_{c'>c} r_c' * e^a costs one ex2 and
+// one rcp per element; row totals of lt come from one lg2 of the product per
+// group of columns (exact slow path if that product underflows).
+constexpr float kProdFloor = 7.52316384526264e-37f;  // 2^-120: lg2 of a normal product is exact enough
+
+// sigma = t/(1+t) and r = 1/(1+t); fminf drops the NaN of inf*0 when t overflows (sigma -> 1)
+__device__ __forceinline__ void sigma_r(float t, float& sg, float& r) {
+  r = rcp(1.0f + t);
+  sg = fminf(t * r, 1.0f);
+}
+
+// Right-to-left pass over n columns of one row: zs[c] holds the raw dot
+// products on entry and Z = z*log2(e) on exit; w[c] = sigma_c * prod_{c<c'<n} r_c',
+// sg[c] = sigma_c (if non-null). Columns c >= lim (diagonal tiles only) are masked:
+// sigma = 0, r = 1. Returns prod r over the group.
+template <int n, bool kDiag>
+__device__ __forceinline__ float prod_pass(float* zs, float* w, float* sg, float scale_log2,
+                                           int c0, int lim) {
+  float Ql = 1.0f;
+#pragma unroll
+  for (int c = n - 1; c >= 0; --c) {
+    const float Z = zs[c] * scale_log2;
+    zs[c] = Z;
+    float s, r;
+    sigma_r(ex2(Z), s, r);
+    if (kDiag) {
+      const bool on = c0 + c < lim;
+      s = on ? s : 0.0f;
+      r = on ? r : 1.0f;
+    }
+    if (sg) sg[c] = s;
+    w[c] = s * Ql;
+    Ql *= r;
+  }
+  return Ql;
+}
+
+// Log-space variant (exact skip path, blocked.py:179-186 restated): Z on exit in
+// zs[c], inclusive in-group suffix sums of lt (log2 units) in cl[c]; returns the
+// group total. Branch-free: masked columns contribute 0.
+template <int n, bool kDiag>
+__device__ __forceinline__ float log_pass(float* zs, float* cl, float scale_log2, int c0, int lim) {
+  float cum = 0.0f;
+#pragma unroll
+  for (int c = n - 1; c >= 0; --c) {
+    const float Z = zs[c] * scale_log2;
+    zs[c] = Z;
+    const float sp = softplus2(Z, ex2(Z));
+    cum -= (!kDiag || c0 + c < lim) ? sp : 0.0f;
+    cl[c] = cum;
+  }
+  return cum;
+}
+
+// log2 of a group's product of r; exact sum of -softplus when it underflowed.
+template <int n, bool kDiag>
+__device__ __forceinline__ float group_log2(float P, const float* Z, int c0, int lim) {
+  if (P >= kProdFloor) return lg2(P);
+  float s = 0.0f;
+#pragma unroll
+  for (int c = 0; c < n; ++c) {
+    const float sp = softplus2(Z[c], ex2(Z[c]));
+    s -= (!kDiag || c0 + c < lim) ? sp : 0.0f;
+  }
+  return s;
+}
+
 }  // namespace sb

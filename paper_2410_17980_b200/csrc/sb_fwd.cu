@@ -38,8 +38,8 @@ struct FwdCfg {
   static constexpr int kOffK = kOffQ + kQBytes;
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffP = kOffV + kStages * kKVBytes;
-  static constexpr int kOffX = kOffP + 2 * kPBytes;         // [2][NG][128] f32 partial sums
-  static constexpr int kOffRed = kOffX + 2 * NG * 128 * 4;  // [2][4] f64 per-warp max(a)
+  static constexpr int kOffX = kOffP + 2 * kPBytes;         // [2][NG][128] f32x2 partials
+  static constexpr int kOffRed = kOffX + 2 * NG * 128 * 8;  // [2][4] f64 per-warp max(a)
   static constexpr int kOffBar = kOffRed + 2 * 4 * 8;
   static constexpr int kNumBars = 1 + 3 * kStages + 2 + 2 + 2 + 2 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   uint32_t* tmem_slot = misc;                                       // TMEM base address
   volatile int* n_eff = reinterpret_cast<volatile int*>(misc + 1);  // tiles the MMA consumes
-  float* xch = reinterpret_cast<float*>(smem + C::kOffX);
+  float2* xch = reinterpret_cast<float2*>(smem + C::kOffX);
   double* red = reinterpret_cast<double*>(smem + C::kOffRed);
 
   if (threadIdx.x == 0) {
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
       const int par = j & 1;
       mbar_wait(bar_sfull + par, (j >> 1) & 1);
       tc_fence_after();
-      float zs[CG], cl[CG];
+      float zs[CG];
       if constexpr (CG == 16) {
         tmem_ld16(tbase + lane_base + C::kColS + par * 64 + c0, zs);
       } else {
@@ -238,21 +238,29 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
       tc_fence_before();
       mbar_arrive(bar_sempty + par);
 
-      // pass 1: softplus and the local (in-group) inclusive suffix sums of lt
+      // pass 1 over this group's columns (right to left). Exact skip path: log
+      // space, exchange the group's sum of lt. Otherwise: product form, exchange
+      // the group's product of r = exp(lt) and its log2.
       const bool mine = act[half] && kb <= my_qb;
-      const int lim = (kb == my_qb) ? (r & 63) : kBlock;  // strict causality on the diagonal
-      float cum = 0.0f;
+      const bool diag = kb == my_qb;  // warp-uniform: a warp's rows share one half
+      const int lim = diag ? (r & 63) : kBlock;  // strict causality on the diagonal
+      float w[CG];
+      float e1 = kSkip ? 0.0f : 1.0f, e2 = 0.0f;
       if (mine) {
-#pragma unroll
-        for (int c = CG - 1; c >= 0; --c) {
-          const float Z = zs[c] * g.scale_log2;
-          const bool on = c0 + c < lim;
-          cum += on ? -softplus2(Z, ex2(Z)) : 0.0f;
-          zs[c] = Z;
-          cl[c] = cum;
+        if constexpr (kSkip) {
+          e1 = diag ? log_pass<CG, true>(zs, w, g.scale_log2, c0, lim)
+                    : log_pass<CG, false>(zs, w, g.scale_log2, c0, lim);
+        } else {
+          if (diag) {
+            e1 = prod_pass<CG, true>(zs, w, nullptr, g.scale_log2, c0, lim);
+            e2 = group_log2<CG, true>(e1, zs, c0, lim);
+          } else {
+            e1 = prod_pass<CG, false>(zs, w, nullptr, g.scale_log2, c0, lim);
+            e2 = group_log2<CG, false>(e1, zs, c0, lim);
+          }
         }
       }
-      xch[(par * NG + gi) * 128 + r] = cum;
+      xch[(par * NG + gi) * 128 + r] = make_float2(e1, e2);
       if (kSkip && gi == 0 && j > 0) {
         // skip check for this tile (blocked.py:175-176), on a after the previous one
         double m = row_valid ? a_d : -INFINITY;
@@ -269,21 +277,33 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
         }
       }
       const bool live = act[half] && kb <= my_qb;
-      float right = 0.0f, tot = 0.0f;  // lt sums of the groups right of mine / of the row
+      // right: what the groups right of mine contribute; tot: the whole row's lt (log2)
+      float right = kSkip ? 0.0f : 1.0f, tot = 0.0f;
 #pragma unroll
       for (int g2 = 0; g2 < NG; ++g2) {
-        const float v = xch[(par * NG + g2) * 128 + r];
-        tot += v;
-        if (g2 > gi) right += v;
+        const float2 v = xch[(par * NG + g2) * 128 + r];
+        if (kSkip) {
+          tot += v.x;
+          if (g2 > gi) right += v.x;
+        } else {
+          tot += v.y;
+          if (g2 > gi) right *= v.x;
+        }
       }
       uint32_t pk[CG / 2];
       if (live) {
-        const float base = right + a2;
+        if constexpr (kSkip) {
+          const float base = right + a2;
 #pragma unroll
-        for (int c = 0; c < CG; c += 2) {
-          const float A0 = (c0 + c < lim) ? ex2(zs[c] + cl[c] + base) : 0.0f;
-          const float A1 = (c0 + c + 1 < lim) ? ex2(zs[c + 1] + cl[c + 1] + base) : 0.0f;
-          pk[c >> 1] = pack_bf16(A0, A1);
+          for (int c = 0; c < CG; c += 2) {
+            const float A0 = (!diag || c0 + c < lim) ? ex2(zs[c] + w[c] + base) : 0.0f;
+            const float A1 = (!diag || c0 + c + 1 < lim) ? ex2(zs[c + 1] + w[c + 1] + base) : 0.0f;
+            pk[c >> 1] = pack_bf16(A0, A1);
+          }
+        } else {
+          const float base = ex2(a2) * right;
+#pragma unroll
+          for (int c = 0; c < CG; c += 2) pk[c >> 1] = pack_bf16(w[c] * base, w[c + 1] * base);
         }
         if (gi == 0 && Mrow && row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
         a_d += (double)tot * (double)kLn2;
