@@ -113,8 +113,11 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   a.counters = tile_counters;
   const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
   a.log_eps = std::log(eps);
-  int rc = sb::fwd_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a,
-                            reinterpret_cast<cudaStream_t>(stream));
+  // skip on: exact log-space kernel (bit-exact skip decisions); skip off: the
+  // ping-pong product-form kernel
+  cudaStream_t st_ = reinterpret_cast<cudaStream_t>(stream);
+  int rc = p->skip ? sb::fwd_dispatch(p->head_dim, true, tq, tk, tv, a, st_)
+                   : sb::fwd_pp_dispatch(p->head_dim, tq, tk, tv, a, st_);
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
 

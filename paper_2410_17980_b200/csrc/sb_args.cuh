@@ -27,6 +27,8 @@ struct BwdArgs {
 
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
                  const CUtensorMap& tv, const BwdArgs& a, int phases, cudaStream_t stream);
+int fwd_pp_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                    const FwdArgs& a, cudaStream_t stream);
 int fwd_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
                  const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
 

@@ -1,0 +1,313 @@
+// Stick-breaking attention forward, ping-pong variant (skip off), sm_100a.
+//
+// Same algorithm as sb_fwd.cu (reference blocked.py:129-206, two_phase=True),
+// organised for throughput: one CTA owns TWO 128-row query tiles of the same
+// (b, h) (tiles 2p and 2p+1, i.e. four reference query blocks) and streams the
+// shared K/V blocks right to left once. Each query tile has its own stick
+// warpgroup (WG0 / WG1, thread r <-> TMEM lane r <-> query row), its own
+// MMA-issuer thread and its own S/P buffers, so the two warpgroups interleave
+// on every SMSP without any cross-warpgroup synchronisation; each thread scans
+// all 64 key columns of its row in registers.
+//
+// Per element (product form, sb_common.cuh): t = 2^Z, r = 1/(1+t), sigma = t*r,
+// A = sigma * (e^a * prod of r to the right), i.e. one ex2 + one rcp.  The
+// row total of lt for `a` is one lg2 of the tile's product of r (exact
+// softplus sum if that product underflows).
+//
+// Warps: 0-3 WG0, 4-7 WG1, 8 TMA producer (+TMEM allocator), 9 MMA for WG0,
+// 10 MMA for WG1.
+#include "sb_args.cuh"
+
+namespace sb {
+
+template <int D>
+struct FwdPPCfg {
+  static constexpr int kStages = D == 128 ? 3 : 4;
+  static constexpr int kThreads = 11 * 32;
+  static constexpr int kQBytes = kTileM * D * 2;
+  static constexpr int kKVBytes = kBlock * D * 2;
+  static constexpr int kPBytes = kTileM * kBlock * 2;
+  static constexpr int kOffQ = 0;                                // Q[2]
+  static constexpr int kOffK = kOffQ + 2 * kQBytes;
+  static constexpr int kOffV = kOffK + kStages * kKVBytes;
+  static constexpr int kOffP = kOffV + kStages * kKVBytes;       // P[wg][buf]
+  static constexpr int kOffBar = kOffP + 4 * kPBytes;
+  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 8 + 2;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
+  static constexpr int kSmem = kOffMisc + 64 + 1024;
+  static constexpr uint32_t kTmemCols = 512;  // S[wg][2] at wg*128 + b*64, O[wg] at 256 + wg*128
+};
+
+template <int D>
+__global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
+    sb_fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const FwdArgs args) {
+  using C = FwdPPCfg<D>;
+  constexpr int ST = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const Geom& g = args.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // heavy-first: pair p covers query tiles 2p (WG0) and 2p+1 (WG1)
+  const int BH = g.B * g.H;
+  const int n_pairs = (g.n_qt + 1) / 2;
+  const int p = n_pairs - 1 - (int)(blockIdx.x / BH);
+  const int bh = (int)(blockIdx.x % BH);
+  const int b = bh / g.H, h = bh % g.H;
+  const bool has1 = 2 * p + 1 < g.n_qt;
+  const int kbhi0 = min(4 * p + 1, g.nb - 1);
+  const int kbhi1 = has1 ? min(4 * p + 3, g.nb - 1) : kbhi0;
+  const int n_s = kbhi1 + 1;  // stream tiles, kb = kbhi1 .. 0
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* bar_q = bars;
+  uint64_t* bar_kfull = bars + 1;
+  uint64_t* bar_vfull = bar_kfull + ST;
+  uint64_t* bar_kvempty = bar_vfull + ST;
+  uint64_t* wgbars = bar_kvempty + ST;  // per wg: sfull[2], sempty[2], pfull[2], pempty[2]
+  uint64_t* bar_ofull = wgbars + 16;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(bar_kfull + s, 1);
+      mbar_init(bar_vfull + s, 1);
+      mbar_init(bar_kvempty + s, has1 ? 2 : 1);
+    }
+    for (int w = 0; w < 2; ++w)
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(wgbars + w * 8 + 0 + s, 1);    // sfull
+        mbar_init(wgbars + w * 8 + 2 + s, 128);  // sempty
+        mbar_init(wgbars + w * 8 + 4 + s, 128);  // pfull
+        mbar_init(wgbars + w * 8 + 6 + s, 1);    // pempty
+      }
+    mbar_init(bar_ofull, 1);
+    mbar_init(bar_ofull + 1, 1);
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_k);
+      tma_prefetch(&tm_v);
+      mbar_expect_tx(bar_q, (has1 ? 2 : 1) * C::kQBytes);
+      for (int w = 0; w < (has1 ? 2 : 1); ++w)
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_4d(&tm_q, bar_q, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128), c * 64,
+                      (2 * p + w) * kTileM, h, b);
+      for (int j = 0; j < n_s; ++j) {
+        const int s = j % ST;
+        if (j >= ST) mbar_wait(bar_kvempty + s, ((j / ST) - 1) & 1);
+        const int kb = kbhi1 - j;
+        mbar_expect_tx(bar_kfull + s, C::kKVBytes);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_4d(&tm_k, bar_kfull + s, smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128),
+                      c * 64, kb * kBlock, h, b);
+        mbar_expect_tx(bar_vfull + s, C::kKVBytes);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
+                      c * 64, kb * kBlock, h, b);
+      }
+    }
+  } else if (warp == 9 || warp == 10) {
+    // ------------------------------------------------------------ MMA issuer of one WG
+    const int w = warp - 9;
+    if (lane == 0 && (w == 0 || has1)) {
+      uint64_t* sfull = wgbars + w * 8;
+      uint64_t* sempty = sfull + 2;
+      uint64_t* pfull = sfull + 4;
+      uint64_t* pempty = sfull + 6;
+      constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T: both K-major
+      constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);   // A V: V is MN-major
+      const uint32_t q_addr = smem_u32(smem + C::kOffQ + w * C::kQBytes);
+      const uint32_t k_addr = smem_u32(smem + C::kOffK);
+      const uint32_t v_addr = smem_u32(smem + C::kOffV);
+      const uint32_t p_addr = smem_u32(smem + C::kOffP + w * 2 * C::kPBytes);
+      const uint32_t tS = tbase + w * 128, tO = tbase + 256 + w * 128;
+      const int j0 = kbhi1 - (w ? kbhi1 : kbhi0);  // first stream tile of this WG
+      const int n_w = n_s - j0;
+      mbar_wait(bar_q, 0);
+      auto issue_pv = [&](int i) {  // local tile i == stream tile j0 + i
+        const int s = (j0 + i) % ST;
+        mbar_wait(pfull + (i & 1), (i >> 1) & 1);
+        mbar_wait(bar_vfull + s, ((j0 + i) / ST) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kBlock / 16; ++k)
+          umma_ss(tO, sdesc_sw128(p_addr + (i & 1) * C::kPBytes + k * 32, 16, 1024),
+                  sdesc_sw128(v_addr + s * C::kKVBytes + k * 2048, kBlock * 128, 1024), idesc_o,
+                  (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(pempty + (i & 1));
+        umma_commit(bar_kvempty + s);
+      };
+      for (int j = 0; j < j0; ++j) {  // stream tiles right of this WG's diagonal
+        mbar_wait(bar_vfull + j % ST, (j / ST) & 1);
+        mbar_arrive(bar_kvempty + j % ST);
+      }
+      for (int i = 0; i < n_w; ++i) {
+        const int j = j0 + i, s = j % ST;
+        mbar_wait(bar_kfull + s, (j / ST) & 1);
+        if (i >= 2) mbar_wait(sempty + (i & 1), ((i >> 1) + 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+          const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+          umma_ss(tS + (i & 1) * 64, sdesc_sw128(q_addr + off, 16, 1024),
+                  sdesc_sw128(k_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(sfull + (i & 1));
+        if (i >= 1) issue_pv(i - 1);
+      }
+      issue_pv(n_w - 1);
+      umma_commit(bar_ofull + w);
+    }
+  } else {
+    // ------------------------------------------------------------ stick warpgroups
+    const int w = warp >> 2;
+    if (w == 0 || has1) {
+      uint64_t* sfull = wgbars + w * 8;
+      uint64_t* sempty = sfull + 2;
+      uint64_t* pfull = sfull + 4;
+      uint64_t* pempty = sfull + 6;
+      const int quarter = warp & 3;
+      const int r = quarter * 32 + lane;
+      const int qt = 2 * p + w;
+      const int my_qb = 2 * qt + (r >> 6);
+      const int row = qt * kTileM + r;
+      const bool row_valid = row < g.L;
+      const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+      const uint32_t tS = tbase + w * 128 + lane_base, tO = tbase + 256 + w * 128 + lane_base;
+      const int64_t unit = (int64_t)b * g.H + h;
+      float* Mrow = args.M + unit * g.n_tiles * kBlock + (r & 63);
+      const uint32_t p_row = smem_u32(smem + C::kOffP + w * 2 * C::kPBytes) + r * 128;
+      const int kbhi = w ? kbhi1 : kbhi0;
+      const int n_w = kbhi + 1;
+      const float sl2 = g.scale_log2;
+      float a2 = 0.0f;  // running log2 remaining mass
+      for (int i = 0; i < n_w; ++i) {
+        const int kb = kbhi - i;
+        mbar_wait(sfull + (i & 1), (i >> 1) & 1);
+        tc_fence_after();
+        float s[64];
+        tmem_ld32(tS + (i & 1) * 64, s);
+        tmem_ld32(tS + (i & 1) * 64 + 32, s + 32);
+        tmem_wait_ld();
+        uint32_t pk[32];
+        bool slow = false;
+        const bool diag = kb == my_qb;
+        const int lim = diag ? (r & 63) : kBlock;
+        if (kb <= my_qb) {  // warp-uniform: a warp's rows share one 64-row half
+          float Ql = ex2(a2), Pr = 1.0f;
+#pragma unroll
+          for (int c = kBlock - 1; c >= 0; c -= 2) {
+            float A[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int cc = c - u;
+              const float Z = fminf(s[cc] * sl2, 126.0f);  // t finite: sigma = t*r <= 1
+              const float t = ex2(Z);
+              float rr = rcp(1.0f + t), sg = t * rr;
+              if (diag && cc >= lim) { rr = 1.0f; sg = 0.0f; }
+              A[u] = sg * Ql;
+              Ql *= rr;
+              Pr *= rr;
+            }
+            pk[(c - 1) >> 1] = pack_bf16(A[1], A[0]);
+          }
+          if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
+          slow = !(Pr >= kProdFloor);
+          if (!slow) a2 += lg2(Pr);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) pk[c] = 0u;
+        }
+        if (__any_sync(0xffffffffu, slow)) {
+          // the tile consumed more than 2^-120 of some row's stick: exact sum of
+          // lt for those rows (S is still in TMEM: s_empty not yet signalled)
+          tmem_ld32(tS + (i & 1) * 64, s);
+          tmem_ld32(tS + (i & 1) * 64 + 32, s + 32);
+          tmem_wait_ld();
+          if (slow) {
+            float lt = 0.0f;
+#pragma unroll
+            for (int c = 0; c < kBlock; ++c) {
+              const float Z = s[c] * sl2;
+              const float sp = softplus2(Z, ex2(Z));
+              lt -= (c < lim) ? sp : 0.0f;
+            }
+            a2 += lt;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(sempty + (i & 1));
+        if (i >= 2) mbar_wait(pempty + (i & 1), ((i >> 1) + 1) & 1);
+        const uint32_t pb = p_row + (i & 1) * C::kPBytes;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          st_shared_v4(pb + ((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                       pk[4 * c + 3]);
+        fence_proxy_async_smem();
+        mbar_arrive(pfull + (i & 1));
+      }
+      // epilogue
+      mbar_wait(bar_ofull + w, 0);
+      tc_fence_after();
+      __nv_bfloat16* orow = args.o + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float ov[32];
+        tmem_ld32(tO + c * 32, ov);
+        tmem_wait_ld();
+        if (row_valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            dst[q4] = make_uint4(pack_bf16(ov[8 * q4], ov[8 * q4 + 1]),
+                                 pack_bf16(ov[8 * q4 + 2], ov[8 * q4 + 3]),
+                                 pack_bf16(ov[8 * q4 + 4], ov[8 * q4 + 5]),
+                                 pack_bf16(ov[8 * q4 + 6], ov[8 * q4 + 7]));
+        }
+      }
+      if (row_valid) args.log_rem[unit * g.L + row] = a2 * kLn2;
+      if (my_qb < g.nb && (r & 63) == 0) {
+        args.first_kb[unit * g.nb + my_qb] = 0;
+        if (args.counters) atomicAdd(args.counters, (unsigned long long)(my_qb + 1));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc<C::kTmemCols>(tbase);
+}
+
+template <int D>
+static int launch_fwd_pp(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                         const FwdArgs& a, cudaStream_t stream) {
+  using C = FwdPPCfg<D>;
+  auto kern = sb_fwd_pp_kernel<D>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  if (e != cudaSuccess) return (int)e;
+  const unsigned grid = (unsigned)(((a.g.n_qt + 1) / 2) * a.g.B * a.g.H);
+  kern<<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, a);
+  return (int)cudaGetLastError();
+}
+
+int fwd_pp_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                    const FwdArgs& a, cudaStream_t stream) {
+  if (D == 128) return launch_fwd_pp<128>(tq, tk, tv, a, stream);
+  if (D == 64) return launch_fwd_pp<64>(tq, tk, tv, a, stream);
+  return -1;
+}
+
+}  // namespace sb
