@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                              ~uintptr_t(1023));
   const Geom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // heaviest pairs first (longest-processing-time order keeps the tail short)
   const int BH = g.B * g.H;
   const int n_pairs = (g.n_qt + 1) / 2;
   const int p = n_pairs - 1 - (int)(blockIdx.x / BH);
@@ -208,9 +209,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t tS = tbase + w * 256, tW = tS + 64, tQ = tS + 128;
       const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
       mbar_wait(bar_qdo, 0);
-      auto issue_dq = [&](int i) {
+      auto issue_dq = [&](int i) {  // inputs landed
         const int s = i % ST;
-        mbar_wait(zfull, i & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kBlock / 16; ++k)
@@ -220,30 +220,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(zempty);
         umma_commit(bar_kvempty + s);
       };
-      for (int j = 0; j < n_w; ++j) {
-        const int s = j % ST;
-        mbar_wait(bar_kfull + s, (j / ST) & 1);
-        mbar_wait(bar_vfull + s, (j / ST) & 1);
-        if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
-        tc_fence_after();
+      // two in-order queues (S and dW, then dQ), issued as their inputs land
+      int is = 0, iq = 0;
+      while (iq < n_w) {
+        const int progress = is + iq;
+        if (is < n_w) {
+          const int s = is % ST;
+          if (mbar_test(bar_kfull + s, (is / ST) & 1) && mbar_test(bar_vfull + s, (is / ST) & 1) &&
+              (is < 1 || mbar_test(sempty, (is - 1) & 1))) {
+            tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-          const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-          umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024),
-                  sdesc_sw128(k_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
-        }
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+              umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024),
+                      sdesc_sw128(k_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
+            }
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-          const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-          umma_ss(tW, sdesc_sw128(do_addr + off, 16, 1024),
-                  sdesc_sw128(v_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+              umma_ss(tW, sdesc_sw128(do_addr + off, 16, 1024),
+                      sdesc_sw128(v_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
+            }
+            umma_commit(sfull);
+            ++is;
+          }
         }
-        umma_commit(sfull);
-        if (j >= 1) issue_dq(j - 1);
+        if (iq < is && mbar_test(zfull, iq & 1)) {
+          issue_dq(iq);
+          ++iq;
+        }
+        if (is + iq == progress) __nanosleep(32);  // nothing ready: yield the SMSP
       }
-      issue_dq(n_w - 1);
       umma_commit(done);
       for (int j = n_w; j < n_s; ++j) {  // stream tiles right of this WG's diagonal
         mbar_wait(bar_vfull + j % ST, (j / ST) & 1);
@@ -383,8 +392,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                              ~uintptr_t(1023));
   const Geom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // small key blocks first: they own the longest columns (LPT order)
   const int BH = g.B * g.H;
-  const int p = (int)(blockIdx.x / BH);  // small key blocks first: they own the longest columns
+  const int p = (int)(blockIdx.x / BH);
   const int bh = (int)(blockIdx.x % BH);
   const int b = bh / g.H, h = bh % g.H;
   const int64_t unit = (int64_t)b * g.H + h;
@@ -469,50 +479,62 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t az_addr = smem_u32(smem + C::kOffAZ + w * C::kPBytes);
       const uint32_t tS = tbase + w * 256, tW = tS + 64, tV = tS + 128, tK = tS + 192;
       mbar_wait(bar_kv, 0);
-      auto finish = [&](int i) {  // dV^T += dO_i^T A_i, then dK^T += Q_i^T dZ_i
-        const int s = i % ST;
-        const uint32_t qa = q0_addr + s * 2 * C::kQBytes, da = qa + C::kQBytes;
-        mbar_wait(afull, i & 1);
-        tc_fence_after();
+      int n = 0;
+      for (int qt = qt_first; qt < g.n_qt; qt = next_live_qt(fkb, g.nb, g.n_qt, kb0, qt + 1)) ++n;
+      // three in-order queues (S and dW; dV^T += dO^T A; dK^T += Q^T dZ), issued
+      // as their inputs land
+      int is = 0, iv = 0, ik = 0;
+      while (ik < n) {
+        const int progress = is + iv + ik;
+        if (is < n) {
+          const int s = is % ST;
+          if (mbar_test(bar_qfull + s, (is / ST) & 1) && (is < 1 || mbar_test(sempty, (is - 1) & 1))) {
+            const uint32_t qa = q0_addr + s * 2 * C::kQBytes, da = qa + C::kQBytes;
+            tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < kTileM / 16; ++k)
-          umma_ss(tV, sdesc_sw128(da + k * 2048, kTileM * 128, 1024),
-                  sdesc_sw128(az_addr + k * 2048, 16, 1024), idesc_t, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(aused);
-        mbar_wait(zfull, i & 1);
-        tc_fence_after();
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+              umma_ss(tS, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(k_addr + offk, 16, 1024),
+                      idesc_s, k > 0);
+            }
 #pragma unroll
-        for (int k = 0; k < kTileM / 16; ++k)
-          umma_ss(tK, sdesc_sw128(qa + k * 2048, kTileM * 128, 1024),
-                  sdesc_sw128(az_addr + k * 2048, 16, 1024), idesc_t, (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(zused);
-        umma_commit(bar_qempty + s);
-      };
-      int j = 0;
-      for (int qt = qt_first; qt < g.n_qt; qt = next_live_qt(fkb, g.nb, g.n_qt, kb0, qt + 1), ++j) {
-        const int s = j % ST;
-        const uint32_t qa = q0_addr + s * 2 * C::kQBytes, da = qa + C::kQBytes;
-        mbar_wait(bar_qfull + s, (j / ST) & 1);
-        if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-          const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-          umma_ss(tS, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(k_addr + offk, 16, 1024),
-                  idesc_s, k > 0);
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+              umma_ss(tW, sdesc_sw128(da + off, 16, 1024), sdesc_sw128(v_addr + offk, 16, 1024),
+                      idesc_s, k > 0);
+            }
+            umma_commit(sfull);
+            ++is;
+          }
         }
+        if (iv < is && mbar_test(afull, iv & 1)) {
+          const uint32_t da = q0_addr + (iv % ST) * 2 * C::kQBytes + C::kQBytes;
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-          const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-          umma_ss(tW, sdesc_sw128(da + off, 16, 1024), sdesc_sw128(v_addr + offk, 16, 1024),
-                  idesc_s, k > 0);
+          for (int k = 0; k < kTileM / 16; ++k)  // dV^T += dO^T A  (K = query rows)
+            umma_ss(tV, sdesc_sw128(da + k * 2048, kTileM * 128, 1024),
+                    sdesc_sw128(az_addr + k * 2048, 16, 1024), idesc_t,
+                    (iv > 0 || k > 0) ? 1u : 0u);
+          umma_commit(aused);
+          ++iv;
         }
-        umma_commit(sfull);
-        if (j >= 1) finish(j - 1);
+        if (ik < iv && mbar_test(zfull, ik & 1)) {
+          const int s = ik % ST;
+          const uint32_t qa = q0_addr + s * 2 * C::kQBytes;
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < kTileM / 16; ++k)  // dK^T += Q^T dZ
+            umma_ss(tK, sdesc_sw128(qa + k * 2048, kTileM * 128, 1024),
+                    sdesc_sw128(az_addr + k * 2048, 16, 1024), idesc_t,
+                    (ik > 0 || k > 0) ? 1u : 0u);
+          umma_commit(zused);
+          umma_commit(bar_qempty + s);
+          ++ik;
+        }
+        if (is + iv + ik == progress) __nanosleep(32);  // nothing ready: yield the SMSP
       }
-      finish(j - 1);
       umma_commit(done);
     }
   }

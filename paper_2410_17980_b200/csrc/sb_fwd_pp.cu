@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   const Geom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // heavy-first: pair p covers query tiles 2p (WG0) and 2p+1 (WG1)
+  // pair p covers query tiles 2p (WG0) and 2p+1 (WG1); heaviest pairs first
+  // (longest-processing-time order keeps the tail short)
   const int BH = g.B * g.H;
   const int n_pairs = (g.n_qt + 1) / 2;
   const int p = n_pairs - 1 - (int)(blockIdx.x / BH);
