@@ -1,0 +1,96 @@
+"""CPU-side checks of the C ABI library (no GPU needed, no compute calls).
+
+The library must load, export every entry point include/sb_attn.h declares,
+and reject invalid arguments with the status codes that mirror the
+reference's ValueErrors before touching the device.
+"""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2410_17980_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sb_attn.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(sb_\w+)\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2410_17980_b200 import build
+        build.build()
+    return _lib.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    syms = declared_symbols()
+    assert set(syms) >= {"sb_fwd", "sb_bwd", "sb_bwd_phase", "sb_snapshot_elems",
+                         "sb_status_string", "sb_version"}
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(_lib.EXPORTS) == set(syms)
+
+
+def test_version_and_status_strings(lib):
+    assert lib.sb_version() >= 1
+    for code in range(8):
+        assert lib.sb_status_string(code)
+    assert b"(0, 1)" in lib.sb_status_string(2)
+
+
+def _params(**kw):
+    p = _lib.SbParams()
+    p.batch, p.heads, p.seqlen, p.head_dim = kw.get("B", 1), kw.get("H", 2), kw.get("L", 256), kw.get("d", 64)
+    p.stride_h = p.seqlen * p.head_dim
+    p.stride_b = p.heads * p.stride_h
+    p.stride_l = p.head_dim
+    p.block = kw.get("block", 64)
+    p.skip = kw.get("skip", 0)
+    p.skip_eps = kw.get("skip_eps", 0.0)
+    p.scale = 0.0
+    return p
+
+
+def test_snapshot_elems_matches_layout(lib):
+    # M/N: B*H*n_tiles*64 with n_tiles = nb(nb+1)/2 (blocked.py:58-60)
+    p = _params(B=2, H=3, L=200)
+    nb = 4
+    assert lib.sb_snapshot_elems(ctypes.byref(p)) == 2 * 3 * nb * (nb + 1) // 2 * 64
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(d=96), 4),               # head_dim not 64/128
+    (dict(block=32), 3),           # d_block must be 64
+    (dict(L=0), 3),                # seq_len >= 1 (blocked.py:64-65)
+    (dict(skip=1, skip_eps=1.5), 2),  # skip_eps in (0,1) (blocked.py:155-156)
+])
+def test_invalid_arguments_rejected_before_launch(lib, kw, code):
+    p = _params(**kw)
+    dummy = ctypes.c_void_p(16)
+    rc = lib.sb_fwd(ctypes.byref(p), dummy, dummy, dummy, dummy, dummy, dummy, dummy, None, None)
+    assert rc == code
+
+
+def test_missing_snapshots_rejected(lib):
+    """blocked.py:315-316: two-phase backward without M snapshots is an error."""
+    p = _params()
+    d = ctypes.c_void_p(16)
+    rc = lib.sb_bwd(ctypes.byref(p), d, d, d, d, None, d, d, None, d, d, d, d, None)
+    assert rc == 5
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+
+
+def test_python_op_refuses_cpu_tensors():
+    import torch
+    import paper_2410_17980_b200 as sb
+    q = torch.zeros(1, 1, 8, 64, dtype=torch.bfloat16)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        sb.stickbreaking_attention(q, q, q)
