@@ -83,6 +83,8 @@ sb::Geom geom(const sb_params_t* p) {
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+uint32_t* g_trace = nullptr;  // SB_TRACE builds: set by sb_debug_set_trace
+
 }  // namespace
 
 extern "C" {
@@ -153,6 +155,7 @@ int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void*
   a.first_kb = first_kb;
   a.M = M;
   a.N = N;
+  a.trace = g_trace;
   int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, a, phases,
                             reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
@@ -174,5 +177,10 @@ const char* sb_status_string(int s) {
 }
 
 int sb_version(void) { return 1; }
+
+#ifdef SB_TRACE
+// debug builds only: device buffer of kTraceCtas*4*64*16 uint32 clock stamps
+void sb_debug_set_trace(void* buf) { g_trace = reinterpret_cast<uint32_t*>(buf); }
+#endif
 
 }  // extern "C"

@@ -23,7 +23,21 @@ struct BwdArgs {
   const int32_t* first_kb;  // [B,H,nb] from the forward
   const float* M;           // forward snapshots (log2 units)
   float* N;                 // phase-1 b snapshots, read by phase 2
+  uint32_t* trace;          // SB_TRACE builds only (libsbattn_trace.so); null otherwise
 };
+
+// Event timeline for kernel tuning (tools/trace_kernels.py).  Compiled only with
+// -DSB_TRACE: slot = (CTA < kTraceCtas, role < 4, tile < 64, event < 16) -> SM clock.
+constexpr int kTraceCtas = 4;
+#ifdef SB_TRACE
+#define SB_TR(args, role, j, ev)                                                          \
+  do {                                                                                    \
+    if ((args).trace && blockIdx.x < kTraceCtas && (j) < 64)                              \
+      (args).trace[((blockIdx.x * 4 + (role)) * 64 + (j)) * 16 + (ev)] = (uint32_t)clock(); \
+  } while (0)
+#else
+#define SB_TR(args, role, j, ev) do { } while (0)
+#endif
 
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
                  const CUtensorMap& tv, const BwdArgs& a, int phases, cudaStream_t stream);

@@ -26,30 +26,67 @@ namespace sb {
 
 constexpr int kBwdThreads = 12 * 32;  // WG0, WG1 stick; WG2 = producer, MMA0, MMA1, idle
 // setmaxnreg only redistributes the CTA's launch allocation (384 threads x 168
-// registers): 128 x 56 + 256 x 224 == 384 x 168, otherwise .inc blocks forever.
-constexpr int kRegsLaunch = 168, kRegsLow = 56, kRegsHigh = 224;
-static_assert(128 * kRegsLow + 256 * kRegsHigh <= kBwdThreads * kRegsLaunch, "register budget");
+// registers): 128 x low + 256 x high <= 384 x 168, otherwise .inc blocks forever.
+constexpr int kRegsLaunch = 168;
+constexpr int kRegsLowQ = 72, kRegsHighQ = 216;    // phase 1
+constexpr int kRegsLowKV = 88, kRegsHighKV = 208;  // phase 2 (issuer holds more descriptors)
+static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "register budget");
+static_assert(128 * kRegsLowKV + 256 * kRegsHighKV <= kBwdThreads * kRegsLaunch, "register budget");
 
 // Right-to-left recompute of one row of a tile: on entry s[] = raw q.k dot
 // products, on exit s[c] = A_c and sg[c] = sigma_c (both 0 where masked).
 // E = e^M (the M snapshot in linear space).
+// Batched reciprocal per group of 16 columns (see batched_row in sb_common.cuh):
+// with P_i = prod_{k<=i} (1+t_k), u_i = t_i P_{i-1} and one rcp of P_15,
+//   A_i = u_i * (Q/P_15),   sigma_i = u_i / P_i,
+// walking the group right to left with the running 1/P_i (one FFMA per element):
+// 6 FP32 ops + 1 ex2 per element.  A group whose product reaches 2^64 (large
+// logits; t = inf included) falls back to one rcp per element.
 template <bool kDiag>
 __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float E,
                                               int lim) {
-  float Ql = E;
+  float Q = E;
 #pragma unroll
-  for (int c = kBlock - 1; c >= 0; --c) {
-    const float Z = fminf(s[c] * scale_log2, 126.0f);  // t finite: sigma = t*r <= 1
-    const float t = ex2(Z);
-    float r = rcp(1.0f + t), sgm = t * r;
-    if (kDiag && c >= lim) { r = 1.0f; sgm = 0.0f; }
-    s[c] = sgm * Ql;
-    sg[c] = sgm;
-    Ql *= r;
+  for (int g = kBlock / 16 - 1; g >= 0; --g) {
+    float t[16], P[16];
+    float p = 1.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = 16 * g + i;
+      float tt = ex2(s[c] * scale_log2);
+      if (kDiag) tt = c < lim ? tt : 0.0f;
+      t[i] = tt;
+      p = fmaf(p, tt, p);
+      P[i] = p;
+    }
+    if (p < kBatchedMax) {
+      float inv = rcp(p);  // 1/P_15, then 1/P_i walking left
+      const float K = Q * inv;
+#pragma unroll
+      for (int i = 15; i >= 0; --i) {
+        const int c = 16 * g + i;
+        const float u = i ? t[i] * P[i - 1] : t[i];
+        sg[c] = u * inv;
+        s[c] = u * K;
+        inv = fmaf(inv, t[i], inv);
+      }
+      Q = K;
+    } else {
+#pragma unroll
+      for (int i = 15; i >= 0; --i) {
+        const int c = 16 * g + i;
+        const float r = rcp(1.0f + t[i]);
+        const float sgm = fminf(t[i] * r, 1.0f);  // t = inf: NaN -> 1
+        s[c] = sgm * Q;
+        sg[c] = sgm;
+        Q *= r;
+      }
+    }
   }
 }
 
 // dAt = A * (dW - off) with dW streamed from TMEM in 16-column chunks (warp-collective).
+template <bool kOff>
 __device__ __forceinline__ void load_dat(float* s, uint32_t taddr, float off) {
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
@@ -57,22 +94,22 @@ __device__ __forceinline__ void load_dat(float* s, uint32_t taddr, float off) {
     tmem_ld16(taddr + ch * 16, w);
     tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < 16; ++c) s[ch * 16 + c] *= (w[c] - off);
+    for (int c = 0; c < 16; ++c) s[ch * 16 + c] *= kOff ? (w[c] - off) : w[c];
   }
 }
 
-// dZ = dAt - sigma*(prefix(dAt) + b), packed to bf16; returns rowsum(dAt).
+// dZ = dAt - sigma*(prefix(dAt) + b), packed to bf16; returns b + rowsum(dAt).
 __device__ __forceinline__ float dz_row(const float* dat, const float* sg, float b, uint32_t* pk) {
-  float pfx = 0.0f;
+  float x = b;
 #pragma unroll
   for (int c = 0; c < kBlock; c += 2) {
-    pfx += dat[c];
-    const float z0 = dat[c] - sg[c] * (pfx + b);
-    pfx += dat[c + 1];
-    const float z1 = dat[c + 1] - sg[c + 1] * (pfx + b);
+    x += dat[c];
+    const float z0 = fmaf(-sg[c], x, dat[c]);
+    x += dat[c + 1];
+    const float z1 = fmaf(-sg[c + 1], x, dat[c + 1]);
     pk[c >> 1] = pack_bf16(z0, z1);
   }
-  return pfx;
+  return x;
 }
 
 __device__ __forceinline__ void store_row_sw128(uint32_t row_addr, int r, const uint32_t* pk) {
@@ -96,7 +133,7 @@ struct BwdQCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kStages * kKVBytes;  // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 5;
+  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 7;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -117,8 +154,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // heaviest pairs first (longest-processing-time order keeps the tail short)
   const int BH = g.B * g.H;
   const int n_pairs = (g.n_qt + 1) / 2;
-  const int p = n_pairs - 1 - (int)(blockIdx.x / BH);
-  const int bh = (int)(blockIdx.x % BH);
+  int item, bh;
+  grouped_order((int)blockIdx.x, n_pairs, BH, item, bh);
+  const int p = n_pairs - 1 - item;
   const int b = bh / g.H, h = bh % g.H;
   const int64_t unit = (int64_t)b * g.H + h;
   const bool has1 = 2 * p + 1 < g.n_qt;
@@ -134,7 +172,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_kfull = bars + 1;
   uint64_t* bar_vfull = bar_kfull + ST;
   uint64_t* bar_kvempty = bar_vfull + ST;
-  uint64_t* wgbars = bar_kvempty + ST;  // per wg: sfull, sempty, zfull, zempty, done
+  uint64_t* wgbars = bar_kvempty + ST;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   if (threadIdx.x == 0) {
@@ -145,11 +183,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(bar_kvempty + s, has1 ? 2 : 1);
     }
     for (int w = 0; w < 2; ++w) {
-      mbar_init(wgbars + w * 5 + 0, 1);
-      mbar_init(wgbars + w * 5 + 1, 128);
-      mbar_init(wgbars + w * 5 + 2, 128);
-      mbar_init(wgbars + w * 5 + 3, 1);
-      mbar_init(wgbars + w * 5 + 4, 1);
+      mbar_init(wgbars + w * 7 + 0, 1);    // sfull: S = Q K^T landed in TMEM
+      mbar_init(wgbars + w * 7 + 1, 128);  // sempty: S read into registers
+      mbar_init(wgbars + w * 7 + 2, 1);    // wfull: dW = dO V^T landed
+      mbar_init(wgbars + w * 7 + 3, 128);  // wempty: dW read
+      mbar_init(wgbars + w * 7 + 4, 128);  // zfull: dZ in smem
+      mbar_init(wgbars + w * 7 + 5, 1);    // zempty: dQ MMA read dZ
+      mbar_init(wgbars + w * 7 + 6, 1);    // done
     }
     fence_mbar_init();
   }
@@ -160,7 +200,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tbase = *tmem_slot;
 
   if (warp >= 8) {
-    reg_dealloc<kRegsLow>();
+    reg_dealloc<kRegsLowQ>();
   if (warp == 8) {
     if (lane == 0) {
       tma_prefetch(&tm_q);
@@ -192,83 +232,90 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 9 || warp == 10) {
+    // whole warp: uniform control flow and descriptors; one elected lane issues
     const int w = warp - 9;
-    if (lane == 0 && (w == 0 || has1)) {
-      uint64_t* sfull = wgbars + w * 5;
-      uint64_t* sempty = sfull + 1;
-      uint64_t* zfull = sfull + 2;
-      uint64_t* zempty = sfull + 3;
-      uint64_t* done = sfull + 4;
+    if (w == 0 || has1) {
+      uint64_t *sfull = wgbars + w * 7, *sempty = sfull + 1, *wfull = sfull + 2,
+               *wempty = sfull + 3, *zfull = sfull + 4, *zempty = sfull + 5, *done = sfull + 6;
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T, dO V^T
       constexpr uint32_t idesc_q = idesc_bf16(128, D, 0, 1);   // dZ K: K is MN-major
-      const uint32_t q_addr = smem_u32(smem + C::kOffQ + w * C::kQBytes);
-      const uint32_t do_addr = smem_u32(smem + C::kOffDO + w * C::kQBytes);
-      const uint32_t k_addr = smem_u32(smem + C::kOffK);
-      const uint32_t v_addr = smem_u32(smem + C::kOffV);
-      const uint32_t z_addr = smem_u32(smem + C::kOffZ + w * C::kZBytes);
+      const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ + w * C::kQBytes), 16, 1024);
+      const uint64_t ddo = sdesc_sw128(smem_u32(smem + C::kOffDO + w * C::kQBytes), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
+      const uint64_t dkmn = sdesc_sw128(smem_u32(smem + C::kOffK), kBlock * 128, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), 16, 1024);
+      const uint64_t dz = sdesc_sw128(smem_u32(smem + C::kOffZ + w * C::kZBytes), 16, 1024);
       const uint32_t tS = tbase + w * 256, tW = tS + 64, tQ = tS + 128;
       const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
+      const bool leader = elect_one();
       mbar_wait(bar_qdo, 0);
-      auto issue_dq = [&](int i) {  // inputs landed
-        const int s = i % ST;
+      // Static issue order matching the stick warpgroup's event order:
+      // S(j+1) once S(j) was read, dW(j+1) once dW(j) was read, dQ(j) once dZ(j)
+      // is in smem.  S of tile j+1 runs while the warpgroup still works on tile j.
+      auto issue_s = [&](int j) {
+        const int s = j % ST;
+        mbar_wait(bar_kfull + s, (j / ST) & 1);
+        if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
         tc_fence_after();
+        if (leader) {
 #pragma unroll
-        for (int k = 0; k < kBlock / 16; ++k)
-          umma_ss(tQ, sdesc_sw128(z_addr + k * 32, 16, 1024),
-                  sdesc_sw128(k_addr + s * C::kKVBytes + k * 2048, kBlock * 128, 1024), idesc_q,
-                  (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(zempty);
-        umma_commit(bar_kvempty + s);
-      };
-      // two in-order queues (S and dW, then dQ), issued as their inputs land
-      int is = 0, iq = 0;
-      while (iq < n_w) {
-        const int progress = is + iq;
-        if (is < n_w) {
-          const int s = is % ST;
-          if (mbar_test(bar_kfull + s, (is / ST) & 1) && mbar_test(bar_vfull + s, (is / ST) & 1) &&
-              (is < 1 || mbar_test(sempty, (is - 1) & 1))) {
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-              umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024),
-                      sdesc_sw128(k_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
-            }
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-              umma_ss(tW, sdesc_sw128(do_addr + off, 16, 1024),
-                      sdesc_sw128(v_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
-            }
-            umma_commit(sfull);
-            ++is;
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+            umma_ss(tS, desc_add(dq, off), desc_add(dk, s * C::kKVBytes + offk), idesc_s, k > 0);
           }
+          umma_commit(sfull);
         }
-        if (iq < is && mbar_test(zfull, iq & 1)) {
-          issue_dq(iq);
-          ++iq;
+        __syncwarp();
+      };
+      auto issue_w = [&](int j) {
+        const int s = j % ST;
+        mbar_wait(bar_vfull + s, (j / ST) & 1);
+        if (j >= 1) mbar_wait(wempty, (j - 1) & 1);
+        tc_fence_after();
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+            umma_ss(tW, desc_add(ddo, off), desc_add(dv, s * C::kKVBytes + offk), idesc_s, k > 0);
+          }
+          umma_commit(wfull);
         }
-        if (is + iq == progress) __nanosleep(32);  // nothing ready: yield the SMSP
+        __syncwarp();
+      };
+      issue_s(0);
+      issue_w(0);
+      for (int j = 0; j < n_w; ++j) {
+        if (j + 1 < n_w) issue_s(j + 1);
+        if (j + 1 < n_w) issue_w(j + 1);
+        const int s = j % ST;
+        mbar_wait(zfull, j & 1);
+        tc_fence_after();
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < kBlock / 16; ++k)
+            umma_ss(tQ, desc_add(dz, k * 32), desc_add(dkmn, s * C::kKVBytes + k * 2048), idesc_q,
+                    (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(zempty);
+          umma_commit(bar_kvempty + s);
+        }
+        __syncwarp();
       }
-      umma_commit(done);
+      if (leader) umma_commit(done);
+      __syncwarp();
       for (int j = n_w; j < n_s; ++j) {  // stream tiles right of this WG's diagonal
         mbar_wait(bar_vfull + j % ST, (j / ST) & 1);
-        mbar_arrive(bar_kvempty + j % ST);
+        if (leader) mbar_arrive(bar_kvempty + j % ST);
       }
     }
   }
   } else {
-    reg_alloc<kRegsHigh>();
+    reg_alloc<kRegsHighQ>();
     const int w = warp >> 2;
     if (w == 0 || has1) {
-      uint64_t* sfull = wgbars + w * 5;
-      uint64_t* sempty = sfull + 1;
-      uint64_t* zfull = sfull + 2;
-      uint64_t* zempty = sfull + 3;
-      uint64_t* done = sfull + 4;
+      uint64_t *sfull = wgbars + w * 7, *sempty = sfull + 1, *wfull = sfull + 2,
+               *wempty = sfull + 3, *zfull = sfull + 4, *zempty = sfull + 5, *done = sfull + 6;
       const int quarter = warp & 3;
       const int r = quarter * 32 + lane;
       const int qt = 2 * p + w;
@@ -284,33 +331,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       float* Nrow = args.N + unit * g.n_tiles * kBlock + (r & 63);
       const uint32_t z_row = smem_u32(smem + C::kOffZ + w * C::kZBytes) + r * 128;
       const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
+      auto tile_of = [&](int kb) -> int64_t {  // snapshot slot (row 0 of the unit if not live)
+        const bool lv = row_valid && kb >= my_first && kb <= my_qb;
+        return tile_index(lv ? my_qb : 0, lv ? kb : 0) * kBlock;
+      };
+      float Ma = Mrow[tile_of(kb_lo)];  // M of the next tile, loaded one tile ahead
       float bsum = 0.0f;  // running b (blocked.py:342, :354)
       for (int j = 0; j < n_w; ++j) {
         const int kb = kb_lo + j;
         const bool live = row_valid && kb >= my_first && kb <= my_qb;
-        const int64_t t = tile_index(live ? my_qb : 0, live ? kb : 0) * kBlock;
-        const float Ma = Mrow[t];  // issued before the S wait to hide its latency
+        const int64_t t = tile_of(kb);
+        const float E = ex2(Ma);
+        if (j + 1 < n_w) Ma = Mrow[tile_of(kb + 1)];
         mbar_wait(sfull, j & 1);
         tc_fence_after();
         float s[64], sg[64];
         tmem_ld32(tS, s);
         tmem_ld32(tS + 32, s + 32);
         tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
         const bool diag = kb == my_qb;  // warp-uniform
         if (live) {
-          if (diag) recompute_row<true>(s, sg, g.scale_log2, ex2(Ma), r & 63);
-          else recompute_row<false>(s, sg, g.scale_log2, ex2(Ma), kBlock);
+          if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
+          else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
         } else {
 #pragma unroll
           for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
         }
-        load_dat(s, tW, off);
+        mbar_wait(wfull, j & 1);
+        tc_fence_after();
+        if (args.row_offset) load_dat<true>(s, tW, off);
+        else load_dat<false>(s, tW, off);
         tc_fence_before();
-        mbar_arrive(sempty);
+        mbar_arrive(wempty);
         uint32_t pk[32];
         if (live) {
           Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
-          bsum += dz_row(s, sg, bsum, pk);
+          bsum = dz_row(s, sg, bsum, pk);
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
@@ -347,38 +405,65 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ============================================================================
-// Phase 2: dK and dV.  CTA = (b, h, key blocks 2p and 2p+1); query tiles stream.
+// Phase 2: dK and dV.  CTA = (b, h, key blocks 2p and 2p+1 = one 128-key pair);
+// query tiles stream top to bottom.  Warpgroup w owns key block 2p+w (thread r
+// <-> query row r of the tile for the stick math, <-> head-dim index r for the
+// dK^T/dV^T epilogue).  Every MMA spans BOTH key blocks (N = 128 keys): the
+// tensor core's shared-memory operand traffic per FLOP is 2/3 of two N = 64 MMAs
+// (measured: 128x64x16 SS-MMAs are smem-bound at 48 clk, 128x128x16 run at the
+// full 64 clk), and one elected thread issues everything in a fixed order.
+//   S    = Q  [K0;K1]^T   (M=128 rows, N=128 keys)  TMEM cols   0..127
+//   dW   = dO [V0;V1]^T                             TMEM cols 128..255
+//   dV^T += dO^T [A0 A1]  (M=D, N=128 keys, K=128 rows)  cols 256..383
+//   dK^T += Q^T [dZ0 dZ1]                                cols 384..511
 template <int D>
 struct BwdKVCfg {
   static constexpr int kStages = D == 128 ? 2 : 3;
   static constexpr int kQBytes = kTileM * D * 2;
-  static constexpr int kKVBytes = kBlock * D * 2;
-  static constexpr int kPBytes = kTileM * kBlock * 2;
-  static constexpr int kOffK = 0;                               // K[2]
-  static constexpr int kOffV = kOffK + 2 * kKVBytes;            // V[2]
-  static constexpr int kOffQ = kOffV + 2 * kKVBytes;            // stage s: Q, dO
-  static constexpr int kOffAZ = kOffQ + kStages * 2 * kQBytes;  // A then dZ, one per WG
+  static constexpr int kPairBytes = 2 * kBlock * D * 2;  // K (or V) of both key blocks
+  static constexpr int kPBytes = kTileM * kBlock * 2;    // A / dZ of one warpgroup
+  static constexpr int kOffK = 0;                        // chunk c: rows 0..127 = K0;K1
+  static constexpr int kOffV = kOffK + kPairBytes;
+  static constexpr int kOffQ = kOffV + kPairBytes;               // stage s: Q, dO
+  static constexpr int kOffAZ = kOffQ + kStages * 2 * kQBytes;   // WG0 then WG1 (contiguous)
   static constexpr int kOffBar = kOffAZ + 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 * 7;
+  static constexpr int kNumBars = 1 + 2 * kStages + 9;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
-  static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dV^T +128, dK^T +192
+  static constexpr uint32_t kTmemCols = 512;
 };
 
 // a tile (qb, kb) is live when the forward visited it: first_kb[qb] <= kb <= qb
 // (blocked.py:372-373)
 __device__ __forceinline__ bool tile_live(const int* fkb, int nb, int qb, int kb) {
-  return qb < nb && qb >= kb && fkb[qb] <= kb;
+  return qb < nb && kb < nb && qb >= kb && fkb[qb] <= kb;
 }
 
-// first query tile >= qt holding a live tile for key block kb0 or kb0+1
-__device__ __forceinline__ int next_live_qt(const int* fkb, int nb, int n_qt, int kb0, int qt) {
-  for (; qt < n_qt; ++qt)
-    if (tile_live(fkb, nb, 2 * qt, kb0) || tile_live(fkb, nb, 2 * qt + 1, kb0) ||
-        tile_live(fkb, nb, 2 * qt, kb0 + 1) || tile_live(fkb, nb, 2 * qt + 1, kb0 + 1))
-      return qt;
-  return n_qt;
-}
+// Warp-cooperative iterator over the query tiles holding a live tile for key
+// block kb0 or kb0+1: 32 tiles are tested at once (one per lane) and kept as a
+// ballot mask, so the per-tile cost is a find-first-set.  Call convergently.
+struct LiveQt {
+  const int* fkb;
+  int nb, n_qt, kb0, base;
+  uint32_t mask;
+  __device__ __forceinline__ void fill(int from) {
+    base = from;
+    const int qt = from + (int)(threadIdx.x & 31);
+    const bool l = qt < n_qt && (tile_live(fkb, nb, 2 * qt, kb0) || tile_live(fkb, nb, 2 * qt + 1, kb0) ||
+                                 tile_live(fkb, nb, 2 * qt, kb0 + 1) ||
+                                 tile_live(fkb, nb, 2 * qt + 1, kb0 + 1));
+    mask = __ballot_sync(0xffffffffu, l);
+  }
+  __device__ __forceinline__ int next() {
+    while (mask == 0) {
+      if (base + 32 >= n_qt) return n_qt;
+      fill(base + 32);
+    }
+    const int bit = __ffs(mask) - 1;
+    mask &= mask - 1;
+    return base + bit;
+  }
+};
 
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
@@ -394,37 +479,47 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // small key blocks first: they own the longest columns (LPT order)
   const int BH = g.B * g.H;
-  const int p = (int)(blockIdx.x / BH);
-  const int bh = (int)(blockIdx.x % BH);
+  int p, bh;
+  grouped_order((int)blockIdx.x, (g.nb + 1) / 2, BH, p, bh);
   const int b = bh / g.H, h = bh % g.H;
   const int64_t unit = (int64_t)b * g.H + h;
   const int kb0 = 2 * p;
-  const bool has1 = kb0 + 1 < g.nb;
   const int* fkb = args.first_kb + unit * g.nb;
-  const int qt_first = next_live_qt(fkb, g.nb, g.n_qt, kb0, p);
+  LiveQt it{fkb, g.nb, g.n_qt, kb0, 0, 0u};
+  it.fill(p);  // query tile p holds the diagonal of key block 2p
+  const int qt_first = it.next();
+  const bool any = qt_first < g.n_qt;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* bar_kv = bars;
   uint64_t* bar_qfull = bars + 1;
   uint64_t* bar_qempty = bar_qfull + ST;
-  uint64_t* wgbars = bar_qempty + ST;  // per wg: sfull, sempty, afull, aused, zfull, zused, done
+  uint64_t* sfull = bar_qempty + ST;  // S = Q K^T landed in TMEM
+  uint64_t* sempty = sfull + 1;       // S read by both warpgroups
+  uint64_t* wfull = sfull + 2;        // dW = dO V^T landed
+  uint64_t* wempty = sfull + 3;       // dW read
+  uint64_t* afull = sfull + 4;        // A of both warpgroups in smem
+  uint64_t* aused = sfull + 5;        // dV^T MMA read A
+  uint64_t* zfull = sfull + 6;        // dZ in smem
+  uint64_t* zused = sfull + 7;        // dK^T MMA read dZ
+  uint64_t* done = sfull + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   if (threadIdx.x == 0) {
     mbar_init(bar_kv, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_qfull + s, 1);
-      mbar_init(bar_qempty + s, has1 ? 2 : 1);
+      mbar_init(bar_qempty + s, 1);
     }
-    for (int w = 0; w < 2; ++w) {
-      mbar_init(wgbars + w * 7 + 0, 1);    // sfull
-      mbar_init(wgbars + w * 7 + 1, 128);  // sempty
-      mbar_init(wgbars + w * 7 + 2, 128);  // afull
-      mbar_init(wgbars + w * 7 + 3, 1);    // aused (dV^T MMA read A)
-      mbar_init(wgbars + w * 7 + 4, 128);  // zfull
-      mbar_init(wgbars + w * 7 + 5, 1);    // zused (dK^T MMA read dZ)
-      mbar_init(wgbars + w * 7 + 6, 1);    // done
-    }
+    mbar_init(sfull, 1);
+    mbar_init(sempty, 256);
+    mbar_init(wfull, 1);
+    mbar_init(wempty, 256);
+    mbar_init(afull, 256);
+    mbar_init(aused, 1);
+    mbar_init(zfull, 256);
+    mbar_init(zused, 1);
+    mbar_init(done, 1);
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -432,200 +527,247 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const bool any = qt_first < g.n_qt;
+  const uint32_t tS = tbase, tW = tbase + 128, tV = tbase + 256, tK = tbase + 384;
 
   if (warp >= 8) {
-    reg_dealloc<kRegsLow>();
-  if (warp == 8) {
-    if (lane == 0 && any) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_do);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      const int nw = has1 ? 2 : 1;
-      mbar_expect_tx(bar_kv, nw * 2 * C::kKVBytes);
-      for (int w = 0; w < nw; ++w)
-        for (int c = 0; c < D / 64; ++c) {
-          const int kr = (kb0 + w) * kBlock;
-          tma_load_4d(&tm_k, bar_kv, smem + C::kOffK + w * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kr, h, b);
-          tma_load_4d(&tm_v, bar_kv, smem + C::kOffV + w * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kr, h, b);
-        }
-      int j = 0;
-      for (int qt = qt_first; qt < g.n_qt; qt = next_live_qt(fkb, g.nb, g.n_qt, kb0, qt + 1), ++j) {
+    reg_dealloc<kRegsLowKV>();
+    if (warp == 8 && any) {
+      // ---------------------------------------------------------- TMA producer
+      const bool leader = elect_one();
+      if (leader) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_do);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        // both key blocks; rows past L (odd nb) are zero-filled by the TMA
+        mbar_expect_tx(bar_kv, 2 * C::kPairBytes);
+        for (int w = 0; w < 2; ++w)  // the K/V tensor maps have 64-row boxes
+          for (int c = 0; c < D / 64; ++c) {
+            const int off = c * (2 * kBlock * 128) + w * (kBlock * 128);
+            tma_load_4d(&tm_k, bar_kv, smem + C::kOffK + off, c * 64, (kb0 + w) * kBlock, h, b);
+            tma_load_4d(&tm_v, bar_kv, smem + C::kOffV + off, c * 64, (kb0 + w) * kBlock, h, b);
+          }
+      }
+      for (int j = 0, qt = qt_first; qt < g.n_qt; qt = it.next(), ++j) {
         const int s = j % ST;
         if (j >= ST) mbar_wait(bar_qempty + s, ((j / ST) - 1) & 1);
-        uint8_t* qdst = smem + C::kOffQ + s * 2 * C::kQBytes;
-        mbar_expect_tx(bar_qfull + s, 2 * C::kQBytes);
-        for (int c = 0; c < D / 64; ++c) {
-          tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64, qt * kTileM, h, b);
-          tma_load_4d(&tm_do, bar_qfull + s, qdst + C::kQBytes + c * (kTileM * 128), c * 64,
-                      qt * kTileM, h, b);
-        }
-      }
-    }
-  } else if (warp == 9 || warp == 10) {
-    const int w = warp - 9;
-    if (lane == 0 && any && (w == 0 || has1)) {
-      uint64_t* sfull = wgbars + w * 7;
-      uint64_t *sempty = sfull + 1, *afull = sfull + 2, *aused = sfull + 3, *zfull = sfull + 4,
-               *zused = sfull + 5, *done = sfull + 6;
-      constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T, dO V^T
-      constexpr uint32_t idesc_t = idesc_bf16(D, 64, 1, 1);    // dO^T A, Q^T dZ: both MN-major
-      const uint32_t k_addr = smem_u32(smem + C::kOffK + w * C::kKVBytes);
-      const uint32_t v_addr = smem_u32(smem + C::kOffV + w * C::kKVBytes);
-      const uint32_t q0_addr = smem_u32(smem + C::kOffQ);
-      const uint32_t az_addr = smem_u32(smem + C::kOffAZ + w * C::kPBytes);
-      const uint32_t tS = tbase + w * 256, tW = tS + 64, tV = tS + 128, tK = tS + 192;
-      mbar_wait(bar_kv, 0);
-      int n = 0;
-      for (int qt = qt_first; qt < g.n_qt; qt = next_live_qt(fkb, g.nb, g.n_qt, kb0, qt + 1)) ++n;
-      // three in-order queues (S and dW; dV^T += dO^T A; dK^T += Q^T dZ), issued
-      // as their inputs land
-      int is = 0, iv = 0, ik = 0;
-      while (ik < n) {
-        const int progress = is + iv + ik;
-        if (is < n) {
-          const int s = is % ST;
-          if (mbar_test(bar_qfull + s, (is / ST) & 1) && (is < 1 || mbar_test(sempty, (is - 1) & 1))) {
-            const uint32_t qa = q0_addr + s * 2 * C::kQBytes, da = qa + C::kQBytes;
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-              umma_ss(tS, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(k_addr + offk, 16, 1024),
-                      idesc_s, k > 0);
-            }
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-              umma_ss(tW, sdesc_sw128(da + off, 16, 1024), sdesc_sw128(v_addr + offk, 16, 1024),
-                      idesc_s, k > 0);
-            }
-            umma_commit(sfull);
-            ++is;
+        SB_TR(args, 2, j, 12);
+        if (leader) {
+          uint8_t* qdst = smem + C::kOffQ + s * 2 * C::kQBytes;
+          mbar_expect_tx(bar_qfull + s, 2 * C::kQBytes);
+          for (int c = 0; c < D / 64; ++c) {
+            tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64, qt * kTileM, h, b);
+            tma_load_4d(&tm_do, bar_qfull + s, qdst + C::kQBytes + c * (kTileM * 128), c * 64,
+                        qt * kTileM, h, b);
           }
         }
-        if (iv < is && mbar_test(afull, iv & 1)) {
-          const uint32_t da = q0_addr + (iv % ST) * 2 * C::kQBytes + C::kQBytes;
-          tc_fence_after();
+        __syncwarp();
+      }
+    } else if (warp == 9 && any) {
+      // ---------------------------------------------------------- MMA issuer
+      // whole warp: uniform control flow and descriptors; one elected lane issues.
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);  // Q K^T, dO V^T (N = 2 blocks)
+      constexpr uint32_t idesc_t = idesc_bf16(D, 128, 1, 1);    // dO^T A, Q^T dZ: MN-major
+      const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), 16, 1024);
+      const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
+      const uint64_t dqmn = sdesc_sw128(smem_u32(smem + C::kOffQ), kTileM * 128, 1024);
+      const uint64_t daz = sdesc_sw128(smem_u32(smem + C::kOffAZ), C::kPBytes, 1024);
+      const bool leader = elect_one();
+      int n = 1;
+      for (int qt = it.next(); qt < g.n_qt; qt = it.next()) ++n;
+      mbar_wait(bar_kv, 0);
+      // Fixed issue order matching the warpgroups' event order:
+      // dV^T(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1) landed], dW(j+1)
+      // [dW(j) read], dK^T(j) [dZ(j) in smem].
+      auto issue_s = [&](int j) {
+        const uint32_t qo = (j % ST) * 2 * C::kQBytes;
+        mbar_wait(bar_qfull + j % ST, (j / ST) & 1);
+        SB_TR(args, 2, j, 13);
+        if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
+        SB_TR(args, 2, j, 8);
+        tc_fence_after();
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (2 * kBlock * 128) + (k & 3) * 32;
+            umma_ss(tS, desc_add(dq, qo + off), desc_add(dk, offk), idesc_s, k > 0);
+          }
+          umma_commit(sfull);
+        }
+        __syncwarp();
+      };
+      auto issue_w = [&](int j) {  // Q/dO stage already landed (issue_s(j) waited)
+        const uint32_t dof = (j % ST) * 2 * C::kQBytes + C::kQBytes;
+        if (j >= 1) mbar_wait(wempty, (j - 1) & 1);
+        SB_TR(args, 2, j, 10);
+        tc_fence_after();
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (2 * kBlock * 128) + (k & 3) * 32;
+            umma_ss(tW, desc_add(dq, dof + off), desc_add(dv, offk), idesc_s, k > 0);
+          }
+          umma_commit(wfull);
+        }
+        __syncwarp();
+      };
+      issue_s(0);
+      issue_w(0);
+      for (int j = 0; j < n; ++j) {
+        const int s = j % ST;
+        const uint32_t qo = s * 2 * C::kQBytes, dof = qo + C::kQBytes;
+        mbar_wait(afull, j & 1);
+        SB_TR(args, 2, j, 9);
+        tc_fence_after();
+        if (leader) {
 #pragma unroll
           for (int k = 0; k < kTileM / 16; ++k)  // dV^T += dO^T A  (K = query rows)
-            umma_ss(tV, sdesc_sw128(da + k * 2048, kTileM * 128, 1024),
-                    sdesc_sw128(az_addr + k * 2048, 16, 1024), idesc_t,
-                    (iv > 0 || k > 0) ? 1u : 0u);
+            umma_ss(tV, desc_add(dqmn, dof + k * 2048), desc_add(daz, k * 2048), idesc_t,
+                    (j > 0 || k > 0) ? 1u : 0u);
           umma_commit(aused);
-          ++iv;
         }
-        if (ik < iv && mbar_test(zfull, ik & 1)) {
-          const int s = ik % ST;
-          const uint32_t qa = q0_addr + s * 2 * C::kQBytes;
-          tc_fence_after();
+        __syncwarp();
+        if (j + 1 < n) issue_s(j + 1);
+        if (j + 1 < n) issue_w(j + 1);
+        mbar_wait(zfull, j & 1);
+        SB_TR(args, 2, j, 11);
+        tc_fence_after();
+        if (leader) {
 #pragma unroll
           for (int k = 0; k < kTileM / 16; ++k)  // dK^T += Q^T dZ
-            umma_ss(tK, sdesc_sw128(qa + k * 2048, kTileM * 128, 1024),
-                    sdesc_sw128(az_addr + k * 2048, 16, 1024), idesc_t,
-                    (ik > 0 || k > 0) ? 1u : 0u);
+            umma_ss(tK, desc_add(dqmn, qo + k * 2048), desc_add(daz, k * 2048), idesc_t,
+                    (j > 0 || k > 0) ? 1u : 0u);
           umma_commit(zused);
           umma_commit(bar_qempty + s);
-          ++ik;
         }
-        if (is + iv + ik == progress) __nanosleep(32);  // nothing ready: yield the SMSP
+        __syncwarp();
       }
-      umma_commit(done);
+      if (leader) umma_commit(done);
+      __syncwarp();
     }
-  }
   } else {
-    reg_alloc<kRegsHigh>();
+    reg_alloc<kRegsHighKV>();
+    // ------------------------------------------------------------ stick warpgroups
     const int w = warp >> 2;
-    if (w == 0 || has1) {
-      uint64_t* sfull = wgbars + w * 7;
-      uint64_t *sempty = sfull + 1, *afull = sfull + 2, *aused = sfull + 3, *zfull = sfull + 4,
-               *zused = sfull + 5, *done = sfull + 6;
-      const int quarter = warp & 3;
-      const int r = quarter * 32 + lane;
-      const int kb = kb0 + w;
-      const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-      const uint32_t tS = tbase + w * 256 + lane_base, tW = tS + 64, tV = tS + 128, tK = tS + 192;
-      const float* Mbase = args.M + unit * g.n_tiles * kBlock + (r & 63);
-      const float* Nbase = args.N + unit * g.n_tiles * kBlock + (r & 63);
-      const uint32_t az_row = smem_u32(smem + C::kOffAZ + w * C::kPBytes) + r * 128;
-      int j = 0;
-      for (int qt = qt_first; qt < g.n_qt; qt = next_live_qt(fkb, g.nb, g.n_qt, kb0, qt + 1), ++j) {
-        const int my_qb = 2 * qt + (r >> 6);
-        const int row = qt * kTileM + r;
-        const bool live = row < g.L && tile_live(fkb, g.nb, my_qb, kb);
-        const int64_t t = live ? tile_index(my_qb, kb) * kBlock : 0;
-        const float Ma = Mbase[t], Nb = Nbase[t];  // issued before the S wait
-        const float off = (live && args.row_offset) ? args.row_offset[unit * g.L + row] : 0.0f;
-        mbar_wait(sfull, j & 1);
-        tc_fence_after();
-        float s[64], sg[64];
-        tmem_ld32(tS, s);
-        tmem_ld32(tS + 32, s + 32);
-        tmem_wait_ld();
-        const bool diag = kb == my_qb;  // warp-uniform
-        if (live) {
-          if (diag) recompute_row<true>(s, sg, g.scale_log2, ex2(Ma), r & 63);
-          else recompute_row<false>(s, sg, g.scale_log2, ex2(Ma), kBlock);
-        } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int kb = kb0 + w;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tSw = tS + lane_base + w * 64, tWw = tW + lane_base + w * 64;
+    const float* Mbase = args.M + unit * g.n_tiles * kBlock + (r & 63);
+    const float* Nbase = args.N + unit * g.n_tiles * kBlock + (r & 63);
+    const uint32_t az_row = smem_u32(smem + C::kOffAZ + w * C::kPBytes) + r * 128;
+    // Per-tile operands: M (needed first) and the liveness of the next tile are
+    // loaded half a tile ahead; N and the row offset at the top of their own tile
+    // (consumed after the recompute).  Indices are clamped so every load is in
+    // bounds whether or not the tile is live.
+    auto tix = [&](int qt) -> int64_t {
+      const int qb = min(2 * qt + (r >> 6), g.nb - 1);
+      return tile_index(qb, min(kb, qb)) * kBlock;
+    };
+    auto is_live = [&](int qt) -> bool {
+      return qt < g.n_qt && qt * kTileM + r < g.L && tile_live(fkb, g.nb, 2 * qt + (r >> 6), kb);
+    };
+    const bool tr = quarter == 0 && lane == 0;
+    if (tr) SB_TR(args, w, 0, 14);
+    int qt = qt_first;
+    bool live = is_live(qt);
+    float Ma = Mbase[tix(qt)];
+    for (int j = 0; qt < g.n_qt; ++j) {
+      const int my_qb = 2 * qt + (r >> 6);
+      const float Nb = Nbase[tix(qt)];
+      const float off =
+          args.row_offset ? args.row_offset[unit * g.L + min(qt * kTileM + r, g.L - 1)] : 0.0f;
+      const float E = ex2(Ma);
+      if (tr) SB_TR(args, w, j, 0);
+      mbar_wait(sfull, j & 1);
+      tc_fence_after();
+      float s[64], sg[64];
+      tmem_ld32(tSw, s);
+      tmem_ld32(tSw + 32, s + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
+      if (tr) SB_TR(args, w, j, 1);
+      const bool diag = kb == my_qb;  // warp-uniform
+      if (live) {
+        if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
+        else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
+      } else {
 #pragma unroll
-          for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
-        }
-        uint32_t pk[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
-        if (j >= 1) mbar_wait(zused, (j - 1) & 1);  // dK^T of the previous tile read the buffer
-        store_row_sw128(az_row, r, pk);
-        fence_proxy_async_smem();
-        mbar_arrive(afull);
-        load_dat(s, tW, off);  // warp-collective
-        tc_fence_before();
-        mbar_arrive(sempty);
-        if (live) {
-          dz_row(s, sg, Nb, pk);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) pk[c] = 0u;
-        }
-        mbar_wait(aused, j & 1);  // dV^T of this tile read A
-        store_row_sw128(az_row, r, pk);
-        fence_proxy_async_smem();
-        mbar_arrive(zfull);
+        for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
       }
+      if (tr) SB_TR(args, w, j, 2);
+      const int qt_next = it.next();  // warp-collective
+      const bool live_next = is_live(qt_next);
+      const float Ma_next = Mbase[tix(qt_next)];
+      uint32_t pk[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
+      if (j >= 1) mbar_wait(zused, (j - 1) & 1);  // dK^T of the previous tile read the buffer
+      if (tr) SB_TR(args, w, j, 8);
+      store_row_sw128(az_row, r, pk);
+      fence_proxy_async_smem();
+      mbar_arrive(afull);
+      if (tr) SB_TR(args, w, j, 3);
+      mbar_wait(wfull, j & 1);
+      tc_fence_after();
+      if (args.row_offset) load_dat<true>(s, tWw, off);  // warp-collective
+      else load_dat<false>(s, tWw, off);
+      tc_fence_before();
+      mbar_arrive(wempty);
+      if (tr) SB_TR(args, w, j, 4);
+      if (live) {
+        dz_row(s, sg, Nb, pk);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) pk[c] = 0u;
+      }
+      if (tr) SB_TR(args, w, j, 5);
+      mbar_wait(aused, j & 1);  // dV^T of this tile read A
+      if (tr) SB_TR(args, w, j, 6);
+      store_row_sw128(az_row, r, pk);
+      fence_proxy_async_smem();
+      mbar_arrive(zfull);
+      if (tr) SB_TR(args, w, j, 7);
+      qt = qt_next;
+      live = live_next;
+      Ma = Ma_next;
+    }
 
-      // epilogue: dV^T / dK^T in TMEM (lanes = head-dim index, columns = keys of kb).
-      // M = 128: lane r <-> d = r.  M = 64: rows 16q+i live in lanes 32q+i, i < 16.
-      const int dlane = (D == 128) ? r : (lane < 16 ? (quarter * 16 + lane) : -1);
+    // epilogue: dV^T / dK^T in TMEM (lanes = head-dim index, columns = keys of the
+    // pair; this warpgroup writes key block kb = columns w*64 ..).
+    // M = 128: lane r <-> d = r.  M = 64: rows 16q+i live in lanes 32q+i, i < 16.
+    const int dlane = (D == 128) ? r : (lane < 16 ? (quarter * 16 + lane) : -1);
+    if (any) {
+      mbar_wait(done, 0);
+      if (tr) SB_TR(args, w, 0, 15);
+      tc_fence_after();
+    }
+    const float scale = g.scale_log2 * kLn2;
+    const int64_t base = (int64_t)b * g.sb + (int64_t)h * g.sh;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float vv[32], kk[32];
       if (any) {
-        mbar_wait(done, 0);
-        tc_fence_after();
+        tmem_ld32(tV + lane_base + w * 64 + half * 32, vv);
+        tmem_ld32(tK + lane_base + w * 64 + half * 32, kk);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) vv[c] = kk[c] = 0.0f;
       }
-      const float scale = g.scale_log2 * kLn2;
-      const int64_t base = (int64_t)b * g.sb + (int64_t)h * g.sh;
+      if (dlane >= 0 && kb < g.nb) {
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float vv[32], kk[32];
-        if (any) {
-          tmem_ld32(tV + half * 32, vv);
-          tmem_ld32(tK + half * 32, kk);
-          tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) vv[c] = kk[c] = 0.0f;
-        }
-        if (dlane >= 0) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int key = kb * kBlock + half * 32 + c;
-            if (key < g.L) {
-              const int64_t o = base + (int64_t)key * g.sl + dlane;
-              args.dv[o] = __float2bfloat16_rn(vv[c]);
-              args.dk[o] = __float2bfloat16_rn(kk[c] * scale);
-            }
+        for (int c = 0; c < 32; ++c) {
+          const int key = kb * kBlock + half * 32 + c;
+          if (key < g.L) {
+            const int64_t o = base + (int64_t)key * g.sl + dlane;
+            args.dv[o] = __float2bfloat16_rn(vv[c]);
+            args.dk[o] = __float2bfloat16_rn(kk[c] * scale);
           }
         }
       }

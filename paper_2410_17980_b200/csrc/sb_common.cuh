@@ -25,6 +25,19 @@ struct Geom {
   int64_t sb, sh, sl;       // element strides of q/k/v/o/do/dq/dk/dv (last dim contiguous)
 };
 
+// CTA -> (work item, unit): the CTAs of kUnitGroup units run together so that
+// the K/V (or Q/dO) stream each CTA reads is shared by its neighbours in L2 (a
+// unit's 4 x 1 MB inputs are re-read by every CTA of that unit); inside a group
+// item 0 (the heaviest, longest-processing-time first) goes first.
+constexpr int kUnitGroup = 8;
+__device__ __forceinline__ void grouped_order(int cta, int n_items, int BH, int& item, int& unit) {
+  const int grp = cta / (kUnitGroup * n_items);
+  const int rem = cta - grp * kUnitGroup * n_items;
+  const int gsz = min(kUnitGroup, BH - grp * kUnitGroup);
+  item = rem / gsz;
+  unit = grp * kUnitGroup + rem % gsz;
+}
+
 // tile(qb, kb) = qb*(qb+1)/2 + kb, the reference's (qb, kb) snapshot key order
 __device__ __forceinline__ int64_t tile_index(int qb, int kb) {
   return (int64_t)qb * (qb + 1) / 2 + kb;
@@ -84,6 +97,52 @@ __device__ __forceinline__ float prod_pass(float* zs, float* w, float* sg, float
     Ql *= r;
   }
   return Ql;
+}
+
+// Batched-reciprocal product form for one row of a 64-column tile (forward).
+// Within a group of 16 columns, with P_i = prod_{k<=i} (1+t_k):
+//   A_i = sigma_i * Q * prod_{k>i} r_k = t_i * Q * P_{i-1} / P_15,
+// so the group needs ONE rcp (1/P_15) and a running product F = Q/P_15 * P_{i-1}
+// (one FFMA per element) instead of one rcp per element.  Groups run right to
+// left carrying Q (e^a times the product of r to the right).  On exit pk holds
+// A packed to bf16, Q the carry past column 0, and Dhi * Dlo the tile's product
+// of (1+t) (so the row total of lt is -(lg2 Dhi + lg2 Dlo) in log2 units).
+// Returns false when a group product reached 2^64 (large logits): the caller
+// then recomputes that row with the per-element form; values are garbage then.
+// Masked columns (c >= lim, diagonal tiles only) get t = 0: A = 0, r = 1.
+constexpr float kBatchedMax = 1.8446744073709552e19f;  // 2^64
+
+template <bool kDiag>
+__device__ __forceinline__ bool batched_row(const float* s, uint32_t* pk, float scale_log2, int lim,
+                                            float& Q, float& Dhi, float& Dlo) {
+  bool ok = true;
+#pragma unroll
+  for (int g = kBlock / 16 - 1; g >= 0; --g) {
+    float t[16];
+    float P = 1.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = 16 * g + i;
+      float tt = ex2(s[c] * scale_log2);  // t = inf makes P = inf: slow path
+      if (kDiag) tt = c < lim ? tt : 0.0f;
+      t[i] = tt;
+      P = fmaf(P, tt, P);
+    }
+    ok = ok && (P < kBatchedMax);
+    float F = Q * rcp(P);
+    Q = F;
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      const float a0 = t[i] * F;
+      F = fmaf(F, t[i], F);
+      const float a1 = t[i + 1] * F;
+      F = fmaf(F, t[i + 1], F);
+      pk[(16 * g + i) >> 1] = pack_bf16(a0, a1);
+    }
+    if (g >= 2) Dhi *= P;
+    else Dlo *= P;
+  }
+  return ok;
 }
 
 // Log-space variant (exact skip path, blocked.py:179-186 restated): Z on exit in

@@ -64,8 +64,9 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
 
   // heavy-first schedule: the last query tiles have the longest key sweeps
   const int BH = g.B * g.H;
-  const int qt = g.n_qt - 1 - (int)(blockIdx.x / BH);
-  const int bh = (int)(blockIdx.x % BH);
+  int item, bh;
+  grouped_order((int)blockIdx.x, g.n_qt, BH, item, bh);
+  const int qt = g.n_qt - 1 - item;
   const int b = bh / g.H, h = bh % g.H;
   const int qb0 = 2 * qt;
   const int kb_hi = min(qb0 + 1, g.nb - 1);  // diagonal block of the upper (or only) half
@@ -154,10 +155,10 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T: both K-major
       constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);   // A V: V is MN-major
-      const uint32_t q_addr = smem_u32(smem + C::kOffQ);
-      const uint32_t k_addr = smem_u32(smem + C::kOffK);
-      const uint32_t v_addr = smem_u32(smem + C::kOffV);
-      const uint32_t p_addr = smem_u32(smem + C::kOffP);
+      const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), kBlock * 128, 1024);
+      const uint64_t dp = sdesc_sw128(smem_u32(smem + C::kOffP), 16, 1024);
       mbar_wait(bar_q, 0);
       auto issue_pv = [&](int i) -> bool {
         mbar_wait(bar_pfull + (i & 1), (i >> 1) & 1);
@@ -167,8 +168,8 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kBlock / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(p_addr + (i & 1) * C::kPBytes + k * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(v_addr + s * C::kKVBytes + k * 2048, kBlock * 128, 1024);
+          const uint64_t ad = desc_add(dp, (i & 1) * C::kPBytes + k * 32);
+          const uint64_t bd = desc_add(dv, s * C::kKVBytes + k * 2048);
           umma_ss(tbase + C::kColO, ad, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(bar_pempty + (i & 1));
@@ -190,8 +191,8 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
             const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-            const uint64_t ad = sdesc_sw128(q_addr + off, 16, 1024);
-            const uint64_t bd = sdesc_sw128(k_addr + s * C::kKVBytes + offk, 16, 1024);
+            const uint64_t ad = desc_add(dq, off);
+            const uint64_t bd = desc_add(dk, s * C::kKVBytes + offk);
             umma_ss(tbase + C::kColS + (j & 1) * 64, ad, bd, idesc_s, k > 0 ? 1u : 0u);
           }
           umma_commit(bar_sfull + (j & 1));

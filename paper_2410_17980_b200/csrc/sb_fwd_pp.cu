@@ -54,8 +54,9 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   // (longest-processing-time order keeps the tail short)
   const int BH = g.B * g.H;
   const int n_pairs = (g.n_qt + 1) / 2;
-  const int p = n_pairs - 1 - (int)(blockIdx.x / BH);
-  const int bh = (int)(blockIdx.x % BH);
+  int item, bh;
+  grouped_order((int)blockIdx.x, n_pairs, BH, item, bh);
+  const int p = n_pairs - 1 - item;
   const int b = bh / g.H, h = bh % g.H;
   const bool has1 = 2 * p + 1 < g.n_qt;
   const int kbhi0 = min(4 * p + 1, g.nb - 1);
@@ -122,56 +123,65 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     }
   } else if (warp == 9 || warp == 10) {
     // ------------------------------------------------------------ MMA issuer of one WG
+    // The whole warp runs the (uniform) control flow and computes descriptors in
+    // uniform registers; one elected lane issues the MMAs and their commits.
     const int w = warp - 9;
-    if (lane == 0 && (w == 0 || has1)) {
+    if (w == 0 || has1) {
       uint64_t* sfull = wgbars + w * 8;
       uint64_t* sempty = sfull + 2;
       uint64_t* pfull = sfull + 4;
       uint64_t* pempty = sfull + 6;
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T: both K-major
       constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);   // A V: V is MN-major
-      const uint32_t q_addr = smem_u32(smem + C::kOffQ + w * C::kQBytes);
-      const uint32_t k_addr = smem_u32(smem + C::kOffK);
-      const uint32_t v_addr = smem_u32(smem + C::kOffV);
-      const uint32_t p_addr = smem_u32(smem + C::kOffP + w * 2 * C::kPBytes);
+      const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ + w * C::kQBytes), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), kBlock * 128, 1024);
+      const uint64_t dp = sdesc_sw128(smem_u32(smem + C::kOffP + w * 2 * C::kPBytes), 16, 1024);
       const uint32_t tS = tbase + w * 128, tO = tbase + 256 + w * 128;
       const int j0 = kbhi1 - (w ? kbhi1 : kbhi0);  // first stream tile of this WG
       const int n_w = n_s - j0;
+      const bool leader = elect_one();
       mbar_wait(bar_q, 0);
       auto issue_pv = [&](int i) {  // local tile i == stream tile j0 + i
         const int s = (j0 + i) % ST;
         mbar_wait(pfull + (i & 1), (i >> 1) & 1);
         mbar_wait(bar_vfull + s, ((j0 + i) / ST) & 1);
         tc_fence_after();
+        if (leader) {
 #pragma unroll
-        for (int k = 0; k < kBlock / 16; ++k)
-          umma_ss(tO, sdesc_sw128(p_addr + (i & 1) * C::kPBytes + k * 32, 16, 1024),
-                  sdesc_sw128(v_addr + s * C::kKVBytes + k * 2048, kBlock * 128, 1024), idesc_o,
-                  (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit(pempty + (i & 1));
-        umma_commit(bar_kvempty + s);
+          for (int k = 0; k < kBlock / 16; ++k)
+            umma_ss(tO, desc_add(dp, (i & 1) * C::kPBytes + k * 32),
+                    desc_add(dv, s * C::kKVBytes + k * 2048), idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(pempty + (i & 1));
+          umma_commit(bar_kvempty + s);
+        }
+        __syncwarp();
       };
       for (int j = 0; j < j0; ++j) {  // stream tiles right of this WG's diagonal
         mbar_wait(bar_vfull + j % ST, (j / ST) & 1);
-        mbar_arrive(bar_kvempty + j % ST);
+        if (leader) mbar_arrive(bar_kvempty + j % ST);
       }
       for (int i = 0; i < n_w; ++i) {
         const int j = j0 + i, s = j % ST;
         mbar_wait(bar_kfull + s, (j / ST) & 1);
         if (i >= 2) mbar_wait(sempty + (i & 1), ((i >> 1) + 1) & 1);
         tc_fence_after();
+        if (leader) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-          const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-          umma_ss(tS + (i & 1) * 64, sdesc_sw128(q_addr + off, 16, 1024),
-                  sdesc_sw128(k_addr + s * C::kKVBytes + offk, 16, 1024), idesc_s, k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+            umma_ss(tS + (i & 1) * 64, desc_add(dq, off), desc_add(dk, s * C::kKVBytes + offk),
+                    idesc_s, k > 0);
+          }
+          umma_commit(sfull + (i & 1));
         }
-        umma_commit(sfull + (i & 1));
+        __syncwarp();
         if (i >= 1) issue_pv(i - 1);
       }
       issue_pv(n_w - 1);
-      umma_commit(bar_ofull + w);
+      if (leader) umma_commit(bar_ofull + w);
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ stick warpgroups
@@ -209,26 +219,12 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         const bool diag = kb == my_qb;
         const int lim = diag ? (r & 63) : kBlock;
         if (kb <= my_qb) {  // warp-uniform: a warp's rows share one 64-row half
-          float Ql = ex2(a2), Pr = 1.0f;
-#pragma unroll
-          for (int c = kBlock - 1; c >= 0; c -= 2) {
-            float A[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int cc = c - u;
-              const float Z = fminf(s[cc] * sl2, 126.0f);  // t finite: sigma = t*r <= 1
-              const float t = ex2(Z);
-              float rr = rcp(1.0f + t), sg = t * rr;
-              if (diag && cc >= lim) { rr = 1.0f; sg = 0.0f; }
-              A[u] = sg * Ql;
-              Ql *= rr;
-              Pr *= rr;
-            }
-            pk[(c - 1) >> 1] = pack_bf16(A[1], A[0]);
-          }
+          // batched reciprocal (sb_common.cuh): one rcp per 16 columns
+          float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
+          slow = diag ? !batched_row<true>(s, pk, sl2, lim, Q, Dhi, Dlo)
+                      : !batched_row<false>(s, pk, sl2, kBlock, Q, Dhi, Dlo);
           if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
-          slow = !(Pr >= kProdFloor);
-          if (!slow) a2 += lg2(Pr);
+          if (!slow) a2 -= lg2(Dhi) + lg2(Dlo);
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
@@ -240,12 +236,24 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           tmem_ld32(tS + (i & 1) * 64 + 32, s + 32);
           tmem_wait_ld();
           if (slow) {
-            float lt = 0.0f;
+            // per-element product form for A, exact softplus sum for a
+            float Ql = ex2(a2), lt = 0.0f;
 #pragma unroll
-            for (int c = 0; c < kBlock; ++c) {
-              const float Z = s[c] * sl2;
-              const float sp = softplus2(Z, ex2(Z));
-              lt -= (c < lim) ? sp : 0.0f;
+            for (int c = kBlock - 1; c >= 0; c -= 2) {
+              float A[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int cc = c - u;
+                const float Z = fminf(s[cc] * sl2, 126.0f);  // t finite: sigma = t*r <= 1
+                const float t = ex2(Z);
+                float rr = rcp(1.0f + t), sg = t * rr;
+                const float sp = softplus2(s[cc] * sl2, t);
+                if (cc >= lim) { rr = 1.0f; sg = 0.0f; }
+                lt -= (cc < lim) ? sp : 0.0f;
+                A[u] = sg * Ql;
+                Ql *= rr;
+              }
+              pk[(c - 1) >> 1] = pack_bf16(A[1], A[0]);
             }
             a2 += lt;
           }

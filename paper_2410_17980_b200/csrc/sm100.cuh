@@ -50,8 +50,15 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Blocking wait.  A wait still pending after 2^33 SM clocks (~4 s; a whole
+// kernel takes milliseconds) is a deadlock: trap so the launch fails loudly
+// instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 33)) __trap();
   }
 }
 
@@ -160,6 +167,23 @@ __device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One elected lane of a converged warp (the lowest active lane, so the same lane
+// every time): MMA issue and its commits run under it while the descriptors are
+// computed warp-uniformly (uniform registers, no per-MMA R2UR/ELECT loops).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// Descriptor of (base + bytes) from the descriptor of base: the start-address
+// field is the low 14 bits (address >> 4) and smem addresses stay below 256 KB.
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(

@@ -1,0 +1,70 @@
+#!/usr/bin/env python3
+"""Per-event SM-clock timeline of the backward kernels (tuning aid, GPU only).
+
+Builds/loads libsbattn_trace.so (-DSB_TRACE), runs the C2 workload once, and
+prints, for the first traced CTAs, the per-tile durations between events of the
+stick warpgroups (roles 0/1) and the MMA issuers (roles 2/3).  Writes the raw
+stamps to gpurun_out/trace_<phase>.npy.
+
+    python tools/trace_kernels.py [--phase 2] [--L 4096]
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2410_17980_b200 import _lib, build, ops  # noqa: E402
+
+NCTA, NROLE, NT, NEV = 4, 4, 64, 16
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--phase", type=int, default=2)
+    ap.add_argument("--B", type=int, default=8)
+    ap.add_argument("--H", type=int, default=16)
+    ap.add_argument("--L", type=int, default=4096)
+    ap.add_argument("--D", type=int, default=128)
+    a = ap.parse_args()
+    path = build.build(trace=True)
+    lib = _lib.load(path)
+    _lib._lib = lib  # route the ops through the trace build
+    lib.sb_debug_set_trace.argtypes = [ctypes.c_void_p]
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    q, k, v, do = (torch.randn(a.B, a.H, a.L, a.D, device=dev, generator=g, dtype=torch.bfloat16)
+                   for _ in range(4))
+    tr = torch.zeros(NCTA * NROLE * NT * NEV, dtype=torch.int32, device=dev)
+    o, cache = ops.sb_forward_blocked(q, k, v)
+    for it in range(3):  # warm, then traced
+        if it == 2:
+            lib.sb_debug_set_trace(tr.data_ptr())
+        ops.blocked_backward_twophase(cache, do)
+        torch.cuda.synchronize()
+    lib.sb_debug_set_trace(None)
+    t = tr.cpu().numpy().view(np.uint32).reshape(NCTA, NROLE, NT, NEV).astype(np.int64)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    np.save(os.path.join(ROOT, "gpurun_out", f"trace_p{a.phase}.npy"), t)
+    for c in range(NCTA):
+        base = t[c, 0, 0, 14]
+        print(f"CTA {c}: start->done {t[c, 0, 0, 15] - base} clk")
+        for role in range(NROLE):
+            rows = []
+            for j in range(NT):
+                ev = t[c, role, j]
+                if not ev.any():
+                    continue
+                rows.append((j, [int(x - base) if x else -1 for x in ev]))
+            print(f"  role {role}: {len(rows)} tiles")
+            for j, ev in rows[:6] + rows[-2:]:
+                print(f"    j={j:2d} " + " ".join(f"{e:7d}" for e in ev[:14]))
+
+
+if __name__ == "__main__":
+    main()
