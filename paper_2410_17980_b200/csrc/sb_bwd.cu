@@ -30,57 +30,74 @@ constexpr int kBwdThreads = 12 * 32;  // WG0, WG1 stick; WG2 = producer, MMA0, M
 constexpr int kRegsLaunch = 168;
 constexpr int kRegsLowQ = 72, kRegsHighQ = 216;    // phase 1
 constexpr int kRegsLowKV = 88, kRegsHighKV = 208;  // phase 2 (issuer holds more descriptors)
-static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "register budget");
 static_assert(128 * kRegsLowKV + 256 * kRegsHighKV <= kBwdThreads * kRegsLaunch, "register budget");
+static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "register budget");
 
-// Right-to-left recompute of one row of a tile: on entry s[] = raw q.k dot
-// products, on exit s[c] = A_c and sg[c] = sigma_c (both 0 where masked).
-// E = e^M (the M snapshot in linear space).
+// Recompute of one row of a tile: on entry s[] = raw q.k dot products, on exit
+// s[c] = A_c and sg[c] = sigma_c (both 0 where masked).  E = e^M (the M
+// snapshot in linear space).
 // Batched reciprocal per group of 16 columns (see batched_row in sb_common.cuh):
-// with P_i = prod_{k<=i} (1+t_k), u_i = t_i P_{i-1} and one rcp of P_15,
-//   A_i = u_i * (Q/P_15),   sigma_i = u_i / P_i,
-// walking the group right to left with the running 1/P_i (one FFMA per element):
-// 6 FP32 ops + 1 ex2 per element.  A group whose product reaches 2^64 (large
-// logits; t = inf included) falls back to one rcp per element.
+// with P_i = prod_{k<=i} (1+t_k) (within the group), u_i = t_i P_{i-1} and one
+// rcp of the group total P_15,
+//   A_i = u_i * (Q_g/P_15),   sigma_i = u_i / P_i,
+// where Q_g = E * prod of r over the groups to the right.  Pass 1 (left to
+// right) keeps t in s[] and P in sg[]; pass 2 walks each group right to left
+// with the running 1/P_i (one FFMA per element).  The four groups are
+// independent chains in both passes (only the scalar Q_g links them), so the
+// scheduler can interleave them: 6 FP32 ops + 1 ex2 per element.  A row whose
+// group product reaches 2^64 (large logits; t = inf included) falls back to one
+// rcp per element.
 template <bool kDiag>
 __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float E,
                                               int lim) {
-  float Q = E;
+  constexpr int NG = kBlock / 16;
+  float tot[NG];
 #pragma unroll
-  for (int g = kBlock / 16 - 1; g >= 0; --g) {
-    float t[16], P[16];
-    float p = 1.0f;
+  for (int g = 0; g < NG; ++g) tot[g] = 1.0f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
       const int c = 16 * g + i;
       float tt = ex2(s[c] * scale_log2);
       if (kDiag) tt = c < lim ? tt : 0.0f;
-      t[i] = tt;
-      p = fmaf(p, tt, p);
-      P[i] = p;
+      s[c] = tt;
+      tot[g] = fmaf(tot[g], tt, tot[g]);
+      sg[c] = tot[g];
     }
-    if (p < kBatchedMax) {
-      float inv = rcp(p);  // 1/P_15, then 1/P_i walking left
-      const float K = Q * inv;
+  bool ok = true;
 #pragma unroll
-      for (int i = 15; i >= 0; --i) {
-        const int c = 16 * g + i;
-        const float u = i ? t[i] * P[i - 1] : t[i];
-        sg[c] = u * inv;
-        s[c] = u * K;
-        inv = fmaf(inv, t[i], inv);
-      }
-      Q = K;
-    } else {
+  for (int g = 0; g < NG; ++g) ok = ok && (tot[g] < kBatchedMax);
+  if (ok) {
+    float inv[NG], K[NG];
+    float Q = E;
 #pragma unroll
-      for (int i = 15; i >= 0; --i) {
+    for (int g = NG - 1; g >= 0; --g) {
+      inv[g] = rcp(tot[g]);
+      K[g] = Q * inv[g];
+      Q = K[g];
+    }
+#pragma unroll
+    for (int i = 15; i >= 0; --i)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
         const int c = 16 * g + i;
-        const float r = rcp(1.0f + t[i]);
-        const float sgm = fminf(t[i] * r, 1.0f);  // t = inf: NaN -> 1
-        s[c] = sgm * Q;
-        sg[c] = sgm;
-        Q *= r;
+        const float t = s[c];
+        const float u = i ? t * sg[c - 1] : t;
+        sg[c] = u * inv[g];
+        s[c] = u * K[g];
+        inv[g] = fmaf(inv[g], t, inv[g]);
       }
+  } else {
+    float Q = E;
+#pragma unroll
+    for (int c = kBlock - 1; c >= 0; --c) {
+      const float t = s[c];
+      const float r = rcp(1.0f + t);
+      const float sgm = fminf(t * r, 1.0f);  // t = inf: NaN -> 1
+      s[c] = sgm * Q;
+      sg[c] = sgm;
+      Q *= r;
     }
   }
 }
@@ -99,17 +116,28 @@ __device__ __forceinline__ void load_dat(float* s, uint32_t taddr, float off) {
 }
 
 // dZ = dAt - sigma*(prefix(dAt) + b), packed to bf16; returns b + rowsum(dAt).
+// Two independent prefix chains (column halves); the right half's offset
+// b + sum(left half) is applied afterwards with one FFMA per element.
 __device__ __forceinline__ float dz_row(const float* dat, const float* sg, float b, uint32_t* pk) {
-  float x = b;
+  constexpr int H = kBlock / 2;
+  float xl = b, xr = 0.0f;
+  float zr[H];
 #pragma unroll
-  for (int c = 0; c < kBlock; c += 2) {
-    x += dat[c];
-    const float z0 = fmaf(-sg[c], x, dat[c]);
-    x += dat[c + 1];
-    const float z1 = fmaf(-sg[c + 1], x, dat[c + 1]);
+  for (int c = 0; c < H; c += 2) {
+    xl += dat[c];
+    xr += dat[H + c];
+    const float z0 = fmaf(-sg[c], xl, dat[c]);
+    zr[c] = fmaf(-sg[H + c], xr, dat[H + c]);
+    xl += dat[c + 1];
+    xr += dat[H + c + 1];
+    const float z1 = fmaf(-sg[c + 1], xl, dat[c + 1]);
+    zr[c + 1] = fmaf(-sg[H + c + 1], xr, dat[H + c + 1]);
     pk[c >> 1] = pack_bf16(z0, z1);
   }
-  return x;
+#pragma unroll
+  for (int c = 0; c < H; c += 2)
+    pk[(H + c) >> 1] = pack_bf16(fmaf(-sg[H + c], xl, zr[c]), fmaf(-sg[H + c + 1], xl, zr[c + 1]));
+  return xl + xr;
 }
 
 __device__ __forceinline__ void store_row_sw128(uint32_t row_addr, int r, const uint32_t* pk) {
@@ -341,7 +369,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int kb = kb_lo + j;
         const bool live = row_valid && kb >= my_first && kb <= my_qb;
         const int64_t t = tile_of(kb);
-        const float E = ex2(Ma);
+        const float E = live ? ex2(Ma) : 0.0f;
         if (j + 1 < n_w) Ma = Mrow[tile_of(kb + 1)];
         mbar_wait(sfull, j & 1);
         tc_fence_after();
@@ -352,13 +380,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
         const bool diag = kb == my_qb;  // warp-uniform
-        if (live) {
-          if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
-          else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
-        } else {
-#pragma unroll
-          for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
-        }
+        // dead rows/tiles run the same code with e^M = 0 and b = 0: A = 0, dZ = 0
+        if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
+        else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
         mbar_wait(wfull, j & 1);
         tc_fence_after();
         if (args.row_offset) load_dat<true>(s, tW, off);
@@ -366,13 +390,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         mbar_arrive(wempty);
         uint32_t pk[32];
-        if (live) {
-          Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
-          bsum = dz_row(s, sg, bsum, pk);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) pk[c] = 0u;
-        }
+        if (live) Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
+        const float bnext = dz_row(s, sg, live ? bsum : 0.0f, pk);
+        bsum = live ? bnext : bsum;
         if (j >= 1) mbar_wait(zempty, (j - 1) & 1);
         store_row_sw128(z_row, r, pk);
         fence_proxy_async_smem();
@@ -430,6 +450,7 @@ struct BwdKVCfg {
   static constexpr int kNumBars = 1 + 2 * kStages + 9;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
+  static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
   static constexpr uint32_t kTmemCols = 512;
 };
 
@@ -441,11 +462,14 @@ __device__ __forceinline__ bool tile_live(const int* fkb, int nb, int qb, int kb
 
 // Warp-cooperative iterator over the query tiles holding a live tile for key
 // block kb0 or kb0+1: 32 tiles are tested at once (one per lane) and kept as a
-// ballot mask, so the per-tile cost is a find-first-set.  Call convergently.
+// ballot mask, so the per-tile cost is a find-first-set.  `mine` holds, for the
+// same window, whether tile (2 qt + half, kb) is live for the calling warp's own
+// 64-row half and key block (stick warps), so no per-tile first_kb loads remain.
+// Call convergently.
 struct LiveQt {
   const int* fkb;
-  int nb, n_qt, kb0, base;
-  uint32_t mask;
+  int nb, n_qt, kb0, half, kb, base;
+  uint32_t mask, mine;
   __device__ __forceinline__ void fill(int from) {
     base = from;
     const int qt = from + (int)(threadIdx.x & 31);
@@ -453,6 +477,7 @@ struct LiveQt {
                                  tile_live(fkb, nb, 2 * qt, kb0 + 1) ||
                                  tile_live(fkb, nb, 2 * qt + 1, kb0 + 1));
     mask = __ballot_sync(0xffffffffu, l);
+    mine = __ballot_sync(0xffffffffu, qt < n_qt && tile_live(fkb, nb, 2 * qt + half, kb));
   }
   __device__ __forceinline__ int next() {
     while (mask == 0) {
@@ -462,6 +487,10 @@ struct LiveQt {
     const int bit = __ffs(mask) - 1;
     mask &= mask - 1;
     return base + bit;
+  }
+  // liveness of the tile just returned by next() for this warp's half / key block
+  __device__ __forceinline__ bool mine_live(int qt) const {
+    return qt < n_qt && ((mine >> (qt - base)) & 1u);
   }
 };
 
@@ -485,7 +514,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int64_t unit = (int64_t)b * g.H + h;
   const int kb0 = 2 * p;
   const int* fkb = args.first_kb + unit * g.nb;
-  LiveQt it{fkb, g.nb, g.n_qt, kb0, 0, 0u};
+  // stick warps: half = which 64-row half of the query tile, kb = own key block
+  LiveQt it{fkb, g.nb, g.n_qt, kb0, (warp & 3) >> 1, kb0 + ((warp >> 2) & 1), 0, 0u, 0u};
   it.fill(p);  // query tile p holds the diagonal of key block 2p
   const int qt_first = it.next();
   const bool any = qt_first < g.n_qt;
@@ -661,16 +691,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float* Nbase = args.N + unit * g.n_tiles * kBlock + (r & 63);
     const uint32_t az_row = smem_u32(smem + C::kOffAZ + w * C::kPBytes) + r * 128;
     // Per-tile operands: M (needed first) and the liveness of the next tile are
-    // loaded half a tile ahead; N and the row offset at the top of their own tile
+    // obtained half a tile ahead; N and the row offset at the top of their own tile
     // (consumed after the recompute).  Indices are clamped so every load is in
     // bounds whether or not the tile is live.
     auto tix = [&](int qt) -> int64_t {
       const int qb = min(2 * qt + (r >> 6), g.nb - 1);
       return tile_index(qb, min(kb, qb)) * kBlock;
     };
-    auto is_live = [&](int qt) -> bool {
-      return qt < g.n_qt && qt * kTileM + r < g.L && tile_live(fkb, g.nb, 2 * qt + (r >> 6), kb);
-    };
+    auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < g.L; };
     const bool tr = quarter == 0 && lane == 0;
     if (tr) SB_TR(args, w, 0, 14);
     int qt = qt_first;
@@ -681,7 +709,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float Nb = Nbase[tix(qt)];
       const float off =
           args.row_offset ? args.row_offset[unit * g.L + min(qt * kTileM + r, g.L - 1)] : 0.0f;
-      const float E = ex2(Ma);
+      const float E = live ? ex2(Ma) : 0.0f;  // dead rows/tiles: A = 0, dZ = 0
       if (tr) SB_TR(args, w, j, 0);
       mbar_wait(sfull, j & 1);
       tc_fence_after();
@@ -693,13 +721,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
       if (tr) SB_TR(args, w, j, 1);
       const bool diag = kb == my_qb;  // warp-uniform
-      if (live) {
-        if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
-        else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
-      } else {
-#pragma unroll
-        for (int c = 0; c < kBlock; ++c) s[c] = sg[c] = 0.0f;
-      }
+      if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
+      else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
       if (tr) SB_TR(args, w, j, 2);
       const int qt_next = it.next();  // warp-collective
       const bool live_next = is_live(qt_next);
@@ -720,12 +743,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(wempty);
       if (tr) SB_TR(args, w, j, 4);
-      if (live) {
-        dz_row(s, sg, Nb, pk);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = 0u;
-      }
+      dz_row(s, sg, live ? Nb : 0.0f, pk);
       if (tr) SB_TR(args, w, j, 5);
       mbar_wait(aused, j & 1);  // dV^T of this tile read A
       if (tr) SB_TR(args, w, j, 6);

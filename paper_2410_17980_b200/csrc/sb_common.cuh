@@ -109,39 +109,52 @@ __device__ __forceinline__ float prod_pass(float* zs, float* w, float* sg, float
 // of (1+t) (so the row total of lt is -(lg2 Dhi + lg2 Dlo) in log2 units).
 // Returns false when a group product reached 2^64 (large logits): the caller
 // then recomputes that row with the per-element form; values are garbage then.
+// s[] is overwritten with t (the caller reloads S for the slow path).
 // Masked columns (c >= lim, diagonal tiles only) get t = 0: A = 0, r = 1.
 constexpr float kBatchedMax = 1.8446744073709552e19f;  // 2^64
 
 template <bool kDiag>
-__device__ __forceinline__ bool batched_row(const float* s, uint32_t* pk, float scale_log2, int lim,
+__device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_log2, int lim,
                                             float& Q, float& Dhi, float& Dlo) {
-  bool ok = true;
+  // pass 1: t into s[] and the group products, four independent chains
+  constexpr int NG = kBlock / 16;
+  float P[NG];
 #pragma unroll
-  for (int g = kBlock / 16 - 1; g >= 0; --g) {
-    float t[16];
-    float P = 1.0f;
+  for (int g = 0; g < NG; ++g) P[g] = 1.0f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
       const int c = 16 * g + i;
       float tt = ex2(s[c] * scale_log2);  // t = inf makes P = inf: slow path
       if (kDiag) tt = c < lim ? tt : 0.0f;
-      t[i] = tt;
-      P = fmaf(P, tt, P);
+      s[c] = tt;
+      P[g] = fmaf(P[g], tt, P[g]);
     }
-    ok = ok && (P < kBatchedMax);
-    float F = Q * rcp(P);
-    Q = F;
+  bool ok = true;
 #pragma unroll
-    for (int i = 0; i < 16; i += 2) {
-      const float a0 = t[i] * F;
-      F = fmaf(F, t[i], F);
-      const float a1 = t[i + 1] * F;
-      F = fmaf(F, t[i + 1], F);
-      pk[(16 * g + i) >> 1] = pack_bf16(a0, a1);
-    }
-    if (g >= 2) Dhi *= P;
-    else Dlo *= P;
+  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < kBatchedMax);
+  // group seeds F_g = Q_g / P_g, right to left
+  float F[NG];
+#pragma unroll
+  for (int g = NG - 1; g >= 0; --g) {
+    F[g] = Q * rcp(P[g]);
+    Q = F[g];
   }
+  // pass 2: A_i = t_i * F, F *= (1 + t_i), four independent chains
+#pragma unroll
+  for (int i = 0; i < 16; i += 2)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int c = 16 * g + i;
+      const float a0 = s[c] * F[g];
+      F[g] = fmaf(F[g], s[c], F[g]);
+      const float a1 = s[c + 1] * F[g];
+      F[g] = fmaf(F[g], s[c + 1], F[g]);
+      pk[c >> 1] = pack_bf16(a0, a1);
+    }
+  Dhi = P[3] * P[2];
+  Dlo = P[1] * P[0];
   return ok;
 }
 

@@ -49,6 +49,12 @@ __global__ void __launch_bounds__(544, 1) ub(int mode, int mma_kind, int nld, un
       mbar_wait(bar, 0);
       out[blockIdx.x * 2 + 0] = clock64() - t0;
     }
+  } else if (warp < nld && mode == 3) {
+    // generic-proxy smem stores (16 B per thread) into 96..160 KB, concurrent with the MMAs
+    uint32_t base = smem_u32(smem + 96 * 1024) + (warp * 32 + lane) * 16;
+    for (int it = 0; it < ITER * 4; ++it)
+      st_shared_v4(base + (it & 7) * 8192, it, it + 1, it + 2, it + 3);
+    if (lane == 0 && warp == 0) out[blockIdx.x * 2 + 1] = clock64() - t0;
   } else if (warp < nld && mode != 1) {
     // loads from columns 256..511 (disjoint from the MMA accumulator at 0..255)
     const uint32_t ta = tb + 256 + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 64 % 256;
@@ -91,7 +97,10 @@ int main() {
       printf("mode %d %-16s nld %2d: MMA %8.0f clk  = %6.1f clk per K=16 MMA, %6.0f FLOP/clk/SM", mode, kn[kind], nld,
              m, m / (8 * ITER), flop / m);
     }
-    if (mode != 1) {
+    if (mode == 3) {
+      double bytes = (double)nld * 32 * 16 * ITER * 4;
+      printf(" | STS (warp 0) %8.0f clk = %6.1f B/clk/SM", l, bytes / l);
+    } else if (mode != 1) {
       double bytes = (double)nld * 32 * 64 * 4 * ITER;
       printf("%s TMEM ld (warp 0) %8.0f clk = %6.1f B/clk/SM", mode >= 1 ? " |" : "mode 0 ", l, bytes / l);
     }
@@ -101,5 +110,7 @@ int main() {
   for (int k = 0; k < 7; ++k) run(1, k, 0);
   for (int nld : {4, 8}) run(2, 0, nld);
   run(2, 1, 8);
+  for (int nld : {4, 8, 16}) run(3, 2, nld);
+  for (int nld : {4, 8, 16}) run(3, 0, nld);
   return 0;
 }
