@@ -277,35 +277,54 @@ def main():
     # ---------------------------------------------------------------- e2e
     e2e = None
     if not args.no_e2e:
+        # Inputs of every step come from pinned host memory; step i+1's H2D copy runs
+        # on a copy stream while step i computes (double-buffered prefetch, as a data
+        # loader would).  Each step ends with a 16-byte D2H read of its checksums.
         hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, d_o))
-        hres = torch.empty(4, dtype=torch.float32).pin_memory()
+        hres = torch.empty(2, 4, dtype=torch.float32).pin_memory()
         h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
-        d2h = hres.numel() * hres.element_size()
-        bufs = [torch.empty_like(q) for _ in range(4)]
+        d2h = hres[0].numel() * hres.element_size()
+        sets = [[torch.empty_like(q) for _ in range(4)] for _ in range(2)]
+        copy_stream = torch.cuda.Stream(device=dev)
+        landed = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step():
-            for buf, hx in zip(bufs, (hq, hk, hv, hdo)):
-                buf.copy_(hx, non_blocking=True)
-            qq, kk, vv = (x.requires_grad_(True) for x in bufs[:3])
-            o = sb.stickbreaking_attention(qq, kk, vv)
-            o.backward(bufs[3])
-            res = torch.stack([o.float().sum(), qq.grad.float().sum(), kk.grad.float().sum(),
-                               vv.grad.float().sum()])
-            hres.copy_(res, non_blocking=True)
-            for x in bufs[:3]:
-                x.grad = None
-                x.requires_grad_(False)
+        def prefetch(i):
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(consumed[i % 2])
+                for buf, hx in zip(sets[i % 2], (hq, hk, hv, hdo)):
+                    buf.copy_(hx, non_blocking=True)
+                landed[i % 2].record(copy_stream)
 
-        for _ in range(2):
-            e2e_step()
+        def e2e_run(n):
+            for c in consumed:
+                c.record(stream)
+            prefetch(0)
+            for i in range(n):
+                if i + 1 < n:
+                    prefetch(i + 1)
+                stream.wait_event(landed[i % 2])
+                bq, bk, bv, bdo = sets[i % 2]
+                qq, kk, vv = (x.requires_grad_(True) for x in (bq, bk, bv))
+                o = sb.stickbreaking_attention(qq, kk, vv)
+                o.backward(bdo)
+                res = torch.stack([o.sum(dtype=torch.float32), qq.grad.sum(dtype=torch.float32),
+                                   kk.grad.sum(dtype=torch.float32),
+                                   vv.grad.sum(dtype=torch.float32)])
+                hres[i % 2].copy_(res, non_blocking=True)
+                consumed[i % 2].record(stream)
+                for x in (qq, kk, vv):
+                    x.grad = None
+                    x.requires_grad_(False)
+
+        e2e_run(2)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        Ke = max(3, min(K, 8))
         a, bev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        Ke = max(2, min(K, 5))
         a.record(stream)
-        for _ in range(Ke):
-            e2e_step()
+        e2e_run(Ke)
         bev.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([a.elapsed_time(bev)], device=dev, dtype=torch.float64)
@@ -314,7 +333,10 @@ def main():
         e2e = {"value": world * B * L * Ke / (te.item() / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": te.item() / Ke,
-               "api": "stickbreaking_attention(q,k,v) + o.backward(dO), pinned host buffers"}
+               "api": "stickbreaking_attention(q,k,v) + o.backward(dO); q,k,v,dO copied from "
+                      "pinned host memory every step (next step's copy overlapped with this "
+                      "step's compute on a copy stream), checksums read back every step",
+               "h2d_gbps": h2d * Ke / (te.item() / 1e3) / 1e9}
 
     # ---------------------------------------------------------------- comparators
     comparator = None
