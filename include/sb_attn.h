@@ -16,6 +16,8 @@
  *                                row_offset)     -> (d_q, d_k, d_v, n_stored)
  *   sb_bwd_phase blocked.py:337-357 / :367-386, the two phases of sb_bwd
  *   sb_snapshot_elems  blocked.py:58-60 BlockLayout.n_tiles x d_block (M/N size)
+ *   sb_varlen_elems    the same sizes for a packed variable-length batch (each
+ *                      sequence planned separately)
  *   sb_status_string   the ValueError messages of blocked.py:115-119, :155-156,
  *                      :246-247, :315-316, :398-399
  */
@@ -35,7 +37,7 @@ enum {
   SB_ERR_SHAPE = 1,        /* q/k/v/d_o shape or stride mismatch (blocked.py:116-119, :246) */
   SB_ERR_SKIP_EPS = 2,     /* skip_eps outside (0, 1) (blocked.py:155-156) */
   SB_ERR_BLOCK = 3,        /* d_block != 64 or seq_len < 1 (blocked.py:64-65) */
-  SB_ERR_UNSUPPORTED = 4,  /* head_dim not in {64, 128}, varlen, non-16B-aligned strides */
+  SB_ERR_UNSUPPORTED = 4,  /* head_dim not in {64, 128}, non-16B-aligned strides */
   SB_ERR_NULL = 5,         /* required pointer is NULL (e.g. missing M, blocked.py:315-316) */
   SB_ERR_DEVICE = 6,       /* no sm_100 device / driver entry point unavailable */
   SB_ERR_LAUNCH = 7        /* CUDA launch or tensor-map encoding failed */
@@ -44,20 +46,37 @@ enum {
 /* Problem description.  q, k, v, o, d_o, dq, dk, dv are bf16 with the element
  * strides below and a contiguous last (head_dim) dimension, e.g. (B, H, L, d)
  * contiguous: stride_b = H*L*d, stride_h = L*d, stride_l = d; or (B, L, H, d):
- * stride_b = L*H*d, stride_l = H*d, stride_h = d. */
+ * stride_b = L*H*d, stride_l = H*d, stride_h = d.
+ *
+ * Packed variable-length batches (cu_seqlens != NULL): the tensors are
+ * (total_tokens, H, d) with token stride stride_l and head stride stride_h
+ * (stride_b unused); sequence b is tokens cu_seqlens[b] .. cu_seqlens[b+1]-1
+ * (cu_seqlens: DEVICE int32 [batch+1], cu_seqlens[0] = 0); seqlen is the
+ * longest sequence (grid sizing).  Every sequence is an independent problem
+ * whose 64-blocks start at its first token.  Per-row outputs (log_rem,
+ * row_offset) are then (total_tokens, H); first_kb and M/N are packed sequence
+ * by sequence, head-major (sizes: sb_varlen_elems). */
 typedef struct sb_params {
   int32_t batch, heads, seqlen, head_dim;
   int64_t stride_b, stride_h, stride_l;
-  const int32_t* cu_seqlens; /* reserved for packed varlen; must be NULL in this version */
+  const int32_t* cu_seqlens; /* NULL: uniform batch; else packed varlen (device pointer) */
   float scale;               /* logit scale; 0 selects 1/sqrt(head_dim) (blocked.py:159) */
   int32_t block;             /* skip / snapshot granularity; must be 64 (blocked.py:41) */
   int32_t skip;              /* enable block skipping (blocked.py:175-176) */
   float skip_eps;            /* in (0, 1); 0 selects 1e-6 (blocked.py:43) */
+  int32_t total_tokens;      /* varlen only: rows of the packed tensors */
 } sb_params_t;
 
 /* Number of float elements of ONE snapshot array (M or N):
  * batch * heads * n_tiles * 64 with n_tiles = nb*(nb+1)/2, nb = ceil(L/64). */
 size_t sb_snapshot_elems(const sb_params_t* p);
+
+/* Varlen sizes from a HOST copy of cu_seqlens ([batch+1]): *snapshot = floats of
+ * one M/N array (heads * sum_b n_tiles(L_b) * 64), *first_kb = int32 elements
+ * of first_kb (heads * sum_b nb(L_b)).  Returns SB_OK or SB_ERR_SHAPE
+ * (decreasing offsets). */
+int sb_varlen_elems(const sb_params_t* p, const int32_t* cu_seqlens_host, size_t* snapshot,
+                    size_t* first_kb);
 
 /* Forward.  Outputs: o (bf16, q's layout), log_rem [B,H,L] float (natural log of
  * the remaining stick mass, RowLogAccumulator.a), first_kb [B,H,nb] int32

@@ -24,10 +24,12 @@ class SbParams(ctypes.Structure):
         ("cu_seqlens", ctypes.c_void_p),
         ("scale", ctypes.c_float), ("block", ctypes.c_int32),
         ("skip", ctypes.c_int32), ("skip_eps", ctypes.c_float),
+        ("total_tokens", ctypes.c_int32),
     ]
 
 
-EXPORTS = ("sb_fwd", "sb_bwd", "sb_bwd_phase", "sb_snapshot_elems", "sb_status_string", "sb_version")
+EXPORTS = ("sb_fwd", "sb_bwd", "sb_bwd_phase", "sb_snapshot_elems", "sb_varlen_elems",
+           "sb_status_string", "sb_version")
 
 _lib = None
 
@@ -50,6 +52,9 @@ def load(path: str = LIB_PATH):
     PP = ctypes.POINTER(SbParams)
     lib.sb_snapshot_elems.restype = ctypes.c_size_t
     lib.sb_snapshot_elems.argtypes = [PP]
+    lib.sb_varlen_elems.restype = ctypes.c_int
+    lib.sb_varlen_elems.argtypes = [PP, P, ctypes.POINTER(ctypes.c_size_t),
+                                    ctypes.POINTER(ctypes.c_size_t)]
     lib.sb_fwd.restype = ctypes.c_int
     lib.sb_fwd.argtypes = [PP, P, P, P, P, P, P, P, P, P]
     lib.sb_bwd.restype = ctypes.c_int

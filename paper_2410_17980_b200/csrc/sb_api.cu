@@ -30,8 +30,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
   auto fn = encode_fn();
   if (!fn) return SB_ERR_DEVICE;
-  const cuuint64_t dims[4] = {(cuuint64_t)p->head_dim, (cuuint64_t)p->seqlen,
-                              (cuuint64_t)p->heads, (cuuint64_t)p->batch};
+  // varlen: one (total_tokens, H) "batch"; kernels add the sequence's first row
+  const bool vl = p->cu_seqlens != nullptr;
+  const cuuint64_t dims[4] = {(cuuint64_t)p->head_dim,
+                              (cuuint64_t)(vl ? p->total_tokens : p->seqlen),
+                              (cuuint64_t)p->heads, (cuuint64_t)(vl ? 1 : p->batch)};
   // strides of singleton dimensions are never dereferenced; keep them legal
   auto legal = [](int64_t s_el, int n, int64_t fallback) -> cuuint64_t {
     int64_t s = s_el * 2;
@@ -39,8 +42,9 @@ int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
     return (cuuint64_t)s;
   };
   const int64_t fb = (int64_t)p->head_dim * 2 * 16;
-  const cuuint64_t strides[3] = {legal(p->stride_l, p->seqlen, fb), legal(p->stride_h, p->heads, fb),
-                                 legal(p->stride_b, p->batch, fb)};
+  const cuuint64_t strides[3] = {
+      legal(p->stride_l, (int)dims[1], fb), legal(p->stride_h, p->heads, fb),
+      legal(vl ? 0 : p->stride_b, (int)dims[3], fb)};
   const cuuint32_t box[4] = {64, (cuuint32_t)rows, 1, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box,
@@ -51,7 +55,7 @@ int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
 
 int validate(const sb_params_t* p) {
   if (!p) return SB_ERR_NULL;
-  if (p->cu_seqlens) return SB_ERR_UNSUPPORTED;
+  if (p->cu_seqlens && p->total_tokens < 1) return SB_ERR_SHAPE;
   if (p->block != 64) return SB_ERR_BLOCK;
   if (p->seqlen < 1 || p->batch < 1 || p->heads < 1) return SB_ERR_BLOCK;
   if (p->head_dim != 64 && p->head_dim != 128) return SB_ERR_UNSUPPORTED;
@@ -60,7 +64,7 @@ int validate(const sb_params_t* p) {
   for (int64_t s : {p->stride_l, p->stride_h, p->stride_b})
     if (s < 0) return SB_ERR_SHAPE;
   if ((p->stride_l * 2) % 16 || (p->heads > 1 && (p->stride_h * 2) % 16) ||
-      (p->batch > 1 && (p->stride_b * 2) % 16))
+      (!p->cu_seqlens && p->batch > 1 && (p->stride_b * 2) % 16))
     return SB_ERR_UNSUPPORTED;
   return SB_OK;
 }
@@ -78,6 +82,7 @@ sb::Geom geom(const sb_params_t* p) {
   g.sb = p->stride_b;
   g.sh = p->stride_h;
   g.sl = p->stride_l;
+  g.cu = p->cu_seqlens;
   return g;
 }
 
@@ -93,6 +98,22 @@ size_t sb_snapshot_elems(const sb_params_t* p) {
   if (!p || p->seqlen < 1) return 0;
   const size_t nb = (size_t)(p->seqlen + 63) / 64;
   return (size_t)p->batch * p->heads * (nb * (nb + 1) / 2) * 64;
+}
+
+int sb_varlen_elems(const sb_params_t* p, const int32_t* cu, size_t* snapshot,
+                    size_t* first_kb) {
+  if (!p || !cu || !snapshot || !first_kb) return SB_ERR_NULL;
+  size_t tiles = 0, nbs = 0;
+  for (int b = 0; b < p->batch; ++b) {
+    const int L = cu[b + 1] - cu[b];
+    if (L < 0) return SB_ERR_SHAPE;
+    const size_t nb = (size_t)(L + 63) / 64;
+    tiles += nb * (nb + 1) / 2;
+    nbs += nb;
+  }
+  *snapshot = (size_t)p->heads * tiles * 64;
+  *first_kb = (size_t)p->heads * nbs;
+  return SB_OK;
 }
 
 int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, void* o,
@@ -115,6 +136,7 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   a.counters = tile_counters;
   const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
   a.log_eps = std::log(eps);
+  a.trace = g_trace;
   // skip on: exact log-space kernel (bit-exact skip decisions); skip off: the
   // ping-pong product-form kernel
   cudaStream_t st_ = reinterpret_cast<cudaStream_t>(stream);
@@ -168,7 +190,7 @@ const char* sb_status_string(int s) {
     case SB_ERR_SKIP_EPS: return "skip_eps must be in (0, 1)";
     case SB_ERR_BLOCK: return "seq_len, batch, heads must be >= 1 and d_block must be 64";
     case SB_ERR_UNSUPPORTED: return "unsupported configuration (head_dim must be 64 or 128, "
-                                    "16-byte aligned rows and strides, no varlen)";
+                                    "16-byte aligned rows and strides)";
     case SB_ERR_NULL: return "required pointer is NULL (two-phase backward needs M snapshots)";
     case SB_ERR_DEVICE: return "CUDA driver entry point unavailable (no sm_100 device?)";
     case SB_ERR_LAUNCH: return "CUDA launch failed";
@@ -176,7 +198,7 @@ const char* sb_status_string(int s) {
   }
 }
 
-int sb_version(void) { return 1; }
+int sb_version(void) { return 2; }  // 2: packed varlen (cu_seqlens, total_tokens)
 
 #ifdef SB_TRACE
 // debug builds only: device buffer of kTraceCtas*4*64*16 uint32 clock stamps

@@ -12,6 +12,7 @@ struct FwdArgs {
   float* M;              // [B,H,n_tiles,64] a-snapshots (log2 units), nullable
   unsigned long long* counters;  // [2]: visited tiles, total tiles (nullable)
   double log_eps;        // log(skip_eps)
+  uint32_t* trace;       // SB_TRACE builds only (libsbattn_trace.so); null otherwise
 };
 
 struct BwdArgs {

@@ -161,7 +161,7 @@ struct BwdQCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kStages * kKVBytes;  // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 7;
+  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 7 + 1;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -181,16 +181,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // heaviest pairs first (longest-processing-time order keeps the tail short)
   const int BH = g.B * g.H;
-  const int n_pairs = (g.n_qt + 1) / 2;
   int item, bh;
-  grouped_order((int)blockIdx.x, n_pairs, BH, item, bh);
-  const int p = n_pairs - 1 - item;
+  grouped_order((int)blockIdx.x, (g.n_qt + 1) / 2, BH, item, bh);
   const int b = bh / g.H, h = bh % g.H;
-  const int64_t unit = (int64_t)b * g.H + h;
-  const bool has1 = 2 * p + 1 < g.n_qt;
-  const int kbhi0 = min(4 * p + 1, g.nb - 1);
-  const int kbhi1 = has1 ? min(4 * p + 3, g.nb - 1) : kbhi0;
-  const int* fkb = args.first_kb + unit * g.nb;
+  const Unit u = make_unit(g, b, h);
+  const int n_pairs = (u.n_qt + 1) / 2;
+  if (item >= n_pairs) return;  // shorter sequence of a varlen batch: no work
+  const int p = n_pairs - 1 - item;
+  const bool has1 = 2 * p + 1 < u.n_qt;
+  const int kbhi0 = min(4 * p + 1, u.nb - 1);
+  const int kbhi1 = has1 ? min(4 * p + 3, u.nb - 1) : kbhi0;
+  const int* fkb = args.first_kb + u.fkb_off;
   int kb_lo = kbhi1;
   for (int qb = 4 * p; qb <= kbhi1; ++qb) kb_lo = min(kb_lo, fkb[qb]);
   const int n_s = kbhi1 - kb_lo + 1;  // stream tiles, kb = kb_lo .. kbhi1
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(wgbars + w * 7 + 5, 1);    // zempty: dQ MMA read dZ
       mbar_init(wgbars + w * 7 + 6, 1);    // done
     }
+    mbar_init(wgbars + 14, 128);  // stagger: WG0 finished its first recompute
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -241,22 +243,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int c = 0; c < D / 64; ++c) {
           const int row0 = (2 * p + w) * kTileM;
           tma_load_4d(&tm_q, bar_qdo, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
-                      c * 64, row0, h, b);
+                      c * 64, u.trow0 + row0, h, u.tb);
           tma_load_4d(&tm_do, bar_qdo, smem + C::kOffDO + w * C::kQBytes + c * (kTileM * 128),
-                      c * 64, row0, h, b);
+                      c * 64, u.trow0 + row0, h, u.tb);
         }
       for (int j = 0; j < n_s; ++j) {
         const int s = j % ST;
         if (j >= ST) mbar_wait(bar_kvempty + s, ((j / ST) - 1) & 1);
+        SB_TR(args, 2, j, 12);
         const int kb = kb_lo + j;
         mbar_expect_tx(bar_kfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_k, bar_kfull + s, smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kb * kBlock, h, b);
+                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
         mbar_expect_tx(bar_vfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kb * kBlock, h, b);
+                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
       }
     }
   } else if (warp == 9 || warp == 10) {
@@ -283,7 +286,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       auto issue_s = [&](int j) {
         const int s = j % ST;
         mbar_wait(bar_kfull + s, (j / ST) & 1);
+        SB_TR(args, 2 + w, j, 13);
         if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
+        SB_TR(args, 2 + w, j, 8);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -300,6 +305,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int s = j % ST;
         mbar_wait(bar_vfull + s, (j / ST) & 1);
         if (j >= 1) mbar_wait(wempty, (j - 1) & 1);
+        SB_TR(args, 2 + w, j, 10);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -319,6 +325,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (j + 1 < n_w) issue_w(j + 1);
         const int s = j % ST;
         mbar_wait(zfull, j & 1);
+        SB_TR(args, 2 + w, j, 11);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -349,14 +356,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int qt = 2 * p + w;
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
-      const bool row_valid = row < g.L;
-      const bool half_exists = my_qb < g.nb;
-      const int my_first = half_exists ? fkb[my_qb] : g.nb;
+      const bool row_valid = row < u.L;
+      const bool half_exists = my_qb < u.nb;
+      const int my_first = half_exists ? fkb[my_qb] : u.nb;
       const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
       const uint32_t tS = tbase + w * 256 + lane_base, tW = tS + 64, tQ = tS + 128;
-      const float off = (args.row_offset && row_valid) ? args.row_offset[unit * g.L + row] : 0.0f;
-      const float* Mrow = args.M + unit * g.n_tiles * kBlock + (r & 63);
-      float* Nrow = args.N + unit * g.n_tiles * kBlock + (r & 63);
+      const float off =
+          (args.row_offset && row_valid) ? args.row_offset[u.rem_off + row * u.rem_stride] : 0.0f;
+      const float* Mrow = args.M + u.m_off + (r & 63);
+      float* Nrow = args.N + u.m_off + (r & 63);
       const uint32_t z_row = smem_u32(smem + C::kOffZ + w * C::kZBytes) + r * 128;
       const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
       auto tile_of = [&](int kb) -> int64_t {  // snapshot slot (row 0 of the unit if not live)
@@ -365,12 +373,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       float Ma = Mrow[tile_of(kb_lo)];  // M of the next tile, loaded one tile ahead
       float bsum = 0.0f;  // running b (blocked.py:342, :354)
+      const bool tr = quarter == 0 && lane == 0;
+      if (tr) SB_TR(args, w, 0, 14);
       for (int j = 0; j < n_w; ++j) {
         const int kb = kb_lo + j;
         const bool live = row_valid && kb >= my_first && kb <= my_qb;
         const int64_t t = tile_of(kb);
         const float E = live ? ex2(Ma) : 0.0f;
         if (j + 1 < n_w) Ma = Mrow[tile_of(kb + 1)];
+        if (tr) SB_TR(args, w, j, 0);
+        // WG1 starts half a tile behind WG0 so the two warpgroups' latency-bound
+        // phases interleave on each SMSP instead of running in lockstep
+        if (j == 0 && w == 1) mbar_wait(wgbars + 14, 0);
         mbar_wait(sfull, j & 1);
         tc_fence_after();
         float s[64], sg[64];
@@ -379,29 +393,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
+        if (tr) SB_TR(args, w, j, 1);
         const bool diag = kb == my_qb;  // warp-uniform
         // dead rows/tiles run the same code with e^M = 0 and b = 0: A = 0, dZ = 0
         if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
         else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
+        if (tr) SB_TR(args, w, j, 2);
+        if (j == 0 && w == 0) mbar_arrive(wgbars + 14);
         mbar_wait(wfull, j & 1);
         tc_fence_after();
         if (args.row_offset) load_dat<true>(s, tW, off);
         else load_dat<false>(s, tW, off);
         tc_fence_before();
         mbar_arrive(wempty);
+        if (tr) SB_TR(args, w, j, 3);
         uint32_t pk[32];
         if (live) Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
         const float bnext = dz_row(s, sg, live ? bsum : 0.0f, pk);
         bsum = live ? bnext : bsum;
+        if (tr) SB_TR(args, w, j, 4);
         if (j >= 1) mbar_wait(zempty, (j - 1) & 1);
+        if (tr) SB_TR(args, w, j, 5);
         store_row_sw128(z_row, r, pk);
         fence_proxy_async_smem();
         mbar_arrive(zfull);
+        if (tr) SB_TR(args, w, j, 6);
       }
       mbar_wait(done, 0);
+      if (tr) SB_TR(args, w, 0, 15);
       tc_fence_after();
       const float scale = g.scale_log2 * kLn2;
-      __nv_bfloat16* dqrow = args.dq + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl;
+      __nv_bfloat16* dqrow = args.dq + u.out_off + (int64_t)row * g.sl;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         float v[32];
@@ -511,14 +533,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   int p, bh;
   grouped_order((int)blockIdx.x, (g.nb + 1) / 2, BH, p, bh);
   const int b = bh / g.H, h = bh % g.H;
-  const int64_t unit = (int64_t)b * g.H + h;
+  const Unit u = make_unit(g, b, h);
+  if (2 * p >= u.nb) return;  // shorter sequence of a varlen batch: no work
   const int kb0 = 2 * p;
-  const int* fkb = args.first_kb + unit * g.nb;
+  const int* fkb = args.first_kb + u.fkb_off;
   // stick warps: half = which 64-row half of the query tile, kb = own key block
-  LiveQt it{fkb, g.nb, g.n_qt, kb0, (warp & 3) >> 1, kb0 + ((warp >> 2) & 1), 0, 0u, 0u};
+  LiveQt it{fkb, u.nb, u.n_qt, kb0, (warp & 3) >> 1, kb0 + ((warp >> 2) & 1), 0, 0u, 0u};
   it.fill(p);  // query tile p holds the diagonal of key block 2p
   const int qt_first = it.next();
-  const bool any = qt_first < g.n_qt;
+  const bool any = qt_first < u.n_qt;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* bar_kv = bars;
@@ -574,11 +597,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int w = 0; w < 2; ++w)  // the K/V tensor maps have 64-row boxes
           for (int c = 0; c < D / 64; ++c) {
             const int off = c * (2 * kBlock * 128) + w * (kBlock * 128);
-            tma_load_4d(&tm_k, bar_kv, smem + C::kOffK + off, c * 64, (kb0 + w) * kBlock, h, b);
-            tma_load_4d(&tm_v, bar_kv, smem + C::kOffV + off, c * 64, (kb0 + w) * kBlock, h, b);
+            tma_load_4d(&tm_k, bar_kv, smem + C::kOffK + off, c * 64,
+                        u.trow0 + (kb0 + w) * kBlock, h, u.tb);
+            tma_load_4d(&tm_v, bar_kv, smem + C::kOffV + off, c * 64,
+                        u.trow0 + (kb0 + w) * kBlock, h, u.tb);
           }
       }
-      for (int j = 0, qt = qt_first; qt < g.n_qt; qt = it.next(), ++j) {
+      for (int j = 0, qt = qt_first; qt < u.n_qt; qt = it.next(), ++j) {
         const int s = j % ST;
         if (j >= ST) mbar_wait(bar_qempty + s, ((j / ST) - 1) & 1);
         SB_TR(args, 2, j, 12);
@@ -586,9 +611,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           uint8_t* qdst = smem + C::kOffQ + s * 2 * C::kQBytes;
           mbar_expect_tx(bar_qfull + s, 2 * C::kQBytes);
           for (int c = 0; c < D / 64; ++c) {
-            tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64, qt * kTileM, h, b);
+            tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64,
+                        u.trow0 + qt * kTileM, h, u.tb);
             tma_load_4d(&tm_do, bar_qfull + s, qdst + C::kQBytes + c * (kTileM * 128), c * 64,
-                        qt * kTileM, h, b);
+                        u.trow0 + qt * kTileM, h, u.tb);
           }
         }
         __syncwarp();
@@ -605,7 +631,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t daz = sdesc_sw128(smem_u32(smem + C::kOffAZ), C::kPBytes, 1024);
       const bool leader = elect_one();
       int n = 1;
-      for (int qt = it.next(); qt < g.n_qt; qt = it.next()) ++n;
+      for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
       mbar_wait(bar_kv, 0);
       // Fixed issue order matching the warpgroups' event order:
       // dV^T(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1) landed], dW(j+1)
@@ -687,28 +713,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int kb = kb0 + w;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t tSw = tS + lane_base + w * 64, tWw = tW + lane_base + w * 64;
-    const float* Mbase = args.M + unit * g.n_tiles * kBlock + (r & 63);
-    const float* Nbase = args.N + unit * g.n_tiles * kBlock + (r & 63);
+    const float* Mbase = args.M + u.m_off + (r & 63);
+    const float* Nbase = args.N + u.m_off + (r & 63);
     const uint32_t az_row = smem_u32(smem + C::kOffAZ + w * C::kPBytes) + r * 128;
     // Per-tile operands: M (needed first) and the liveness of the next tile are
     // obtained half a tile ahead; N and the row offset at the top of their own tile
     // (consumed after the recompute).  Indices are clamped so every load is in
     // bounds whether or not the tile is live.
     auto tix = [&](int qt) -> int64_t {
-      const int qb = min(2 * qt + (r >> 6), g.nb - 1);
+      const int qb = min(2 * qt + (r >> 6), u.nb - 1);
       return tile_index(qb, min(kb, qb)) * kBlock;
     };
-    auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < g.L; };
+    auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < u.L; };
     const bool tr = quarter == 0 && lane == 0;
     if (tr) SB_TR(args, w, 0, 14);
     int qt = qt_first;
     bool live = is_live(qt);
     float Ma = Mbase[tix(qt)];
-    for (int j = 0; qt < g.n_qt; ++j) {
+    for (int j = 0; qt < u.n_qt; ++j) {
       const int my_qb = 2 * qt + (r >> 6);
       const float Nb = Nbase[tix(qt)];
       const float off =
-          args.row_offset ? args.row_offset[unit * g.L + min(qt * kTileM + r, g.L - 1)] : 0.0f;
+          args.row_offset
+              ? args.row_offset[u.rem_off + min(qt * kTileM + r, u.L - 1) * u.rem_stride]
+              : 0.0f;
       const float E = live ? ex2(Ma) : 0.0f;  // dead rows/tiles: A = 0, dZ = 0
       if (tr) SB_TR(args, w, j, 0);
       mbar_wait(sfull, j & 1);
@@ -766,7 +794,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
     }
     const float scale = g.scale_log2 * kLn2;
-    const int64_t base = (int64_t)b * g.sb + (int64_t)h * g.sh;
+    const int64_t base = u.out_off;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       float vv[32], kk[32];
@@ -778,11 +806,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c) vv[c] = kk[c] = 0.0f;
       }
-      if (dlane >= 0 && kb < g.nb) {
+      if (dlane >= 0 && kb < u.nb) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int key = kb * kBlock + half * 32 + c;
-          if (key < g.L) {
+          if (key < u.L) {
             const int64_t o = base + (int64_t)key * g.sl + dlane;
             args.dv[o] = __float2bfloat16_rn(vv[c]);
             args.dk[o] = __float2bfloat16_rn(kk[c] * scale);

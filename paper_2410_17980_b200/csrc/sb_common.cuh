@@ -18,12 +18,67 @@ constexpr float kSoftplusThr2 = 15.0f * kLog2e;
 // Problem geometry shared by all kernels. Uniform batches: every (b, h) unit is
 // an independent L x d problem.
 struct Geom {
-  int B, H, L, nb;          // nb = ceil(L / 64) key/query blocks
+  int B, H, L, nb;          // nb = ceil(L / 64) key/query blocks (L = max length if varlen)
   int n_qt;                 // ceil(L / 128) query tiles
   int64_t n_tiles;          // nb*(nb+1)/2 lower-triangular 64x64 tiles per unit
   float scale_log2;         // softmax-free logit scale times log2(e)
   int64_t sb, sh, sl;       // element strides of q/k/v/o/do/dq/dk/dv (last dim contiguous)
+  const int32_t* cu;        // varlen: [B+1] sequence offsets into the packed token axis
 };
+
+// One (sequence, head) unit: its length and where its rows, snapshots and
+// per-row outputs live.  Uniform batches: unit = b*H + h, [B,H,L] layouts.
+// Packed variable-length batches (cu != null): sequence b
+// is tokens cu[b] .. cu[b+1]-1 of a (total, H, d) tensor, blocks restart at
+// every sequence start (each sequence is an independent problem, as the
+// reference runs each one separately); M/N/first_kb are packed sequence-major
+// then head-major, log_rem / row_offset are (total, H).
+struct Unit {
+  int L, nb, n_qt;
+  int64_t n_tiles;
+  int trow0, tb;               // TMA coordinates: row offset and batch index
+  int64_t m_off, fkb_off;      // element offsets into M / N and first_kb
+  int64_t rem_off, rem_stride; // log_rem / row_offset element of row r: rem_off + r*rem_stride
+  int64_t out_off;             // element offset of row 0 in q/k/v/o/do/dq/dk/dv
+};
+
+__device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
+  Unit u;
+  if (!g.cu) {
+    const int64_t unit = (int64_t)b * g.H + h;
+    u.L = g.L;
+    u.nb = g.nb;
+    u.n_qt = g.n_qt;
+    u.n_tiles = g.n_tiles;
+    u.trow0 = 0;
+    u.tb = b;
+    u.m_off = unit * g.n_tiles * kBlock;
+    u.fkb_off = unit * g.nb;
+    u.rem_off = unit * g.L;
+    u.rem_stride = 1;
+    u.out_off = (int64_t)b * g.sb + (int64_t)h * g.sh;
+  } else {
+    int64_t tiles_before = 0, nb_before = 0;
+    for (int i = 0; i < b; ++i) {
+      const int nbi = (g.cu[i + 1] - g.cu[i] + kBlock - 1) / kBlock;
+      tiles_before += (int64_t)nbi * (nbi + 1) / 2;
+      nb_before += nbi;
+    }
+    const int s0 = g.cu[b];
+    u.L = g.cu[b + 1] - s0;
+    u.nb = (u.L + kBlock - 1) / kBlock;
+    u.n_qt = (u.L + kTileM - 1) / kTileM;
+    u.n_tiles = (int64_t)u.nb * (u.nb + 1) / 2;
+    u.trow0 = s0;
+    u.tb = 0;
+    u.m_off = (tiles_before * g.H + (int64_t)h * u.n_tiles) * kBlock;
+    u.fkb_off = nb_before * g.H + (int64_t)h * u.nb;
+    u.rem_off = (int64_t)s0 * g.H + h;
+    u.rem_stride = g.H;
+    u.out_off = (int64_t)s0 * g.sl + (int64_t)h * g.sh;
+  }
+  return u;
+}
 
 // CTA -> (work item, unit): the CTAs of kUnitGroup units run together so that
 // the K/V (or Q/dO) stream each CTA reads is shared by its neighbours in L2 (a

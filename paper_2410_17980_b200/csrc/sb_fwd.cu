@@ -66,10 +66,12 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
   const int BH = g.B * g.H;
   int item, bh;
   grouped_order((int)blockIdx.x, g.n_qt, BH, item, bh);
-  const int qt = g.n_qt - 1 - item;
   const int b = bh / g.H, h = bh % g.H;
+  const Unit u = make_unit(g, b, h);
+  if (item >= u.n_qt) return;  // shorter sequence of a varlen batch: no work
+  const int qt = u.n_qt - 1 - item;
   const int qb0 = 2 * qt;
-  const int kb_hi = min(qb0 + 1, g.nb - 1);  // diagonal block of the upper (or only) half
+  const int kb_hi = min(qb0 + 1, u.nb - 1);  // diagonal block of the upper (or only) half
   const int n_kv = kb_hi + 1;                // tiles without skipping (kb = kb_hi .. 0)
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -120,7 +122,8 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
       const int row0 = qt * kTileM;
       mbar_expect_tx(bar_q, C::kQBytes);
       for (int c = 0; c < D / 64; ++c)
-        tma_load_4d(&tm_q, bar_q, smem + C::kOffQ + c * (kTileM * 128), c * 64, row0, h, b);
+        tma_load_4d(&tm_q, bar_q, smem + C::kOffQ + c * (kTileM * 128), c * 64, u.trow0 + row0, h,
+                    u.tb);
       int issued = 0;
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % ST;
@@ -137,11 +140,11 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
         mbar_expect_tx(bar_kfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_k, bar_kfull + s, smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kb * kBlock, h, b);
+                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
         mbar_expect_tx(bar_vfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kb * kBlock, h, b);
+                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
         ++issued;
       }
       // never leave the CTA with bulk copies in flight (early exit under skip)
@@ -212,16 +215,15 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
     const int half = r >> 6;
     const int my_qb = qb0 + half;
     const int row = qt * kTileM + r;
-    const bool row_valid = row < g.L;
+    const bool row_valid = row < u.L;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const int64_t unit = (int64_t)b * g.H + h;
-    float* Mrow = args.M ? args.M + unit * g.n_tiles * kBlock + (r & 63) : nullptr;
+    float* Mrow = args.M ? args.M + u.m_off + (r & 63) : nullptr;
     const uint32_t p_row = smem_u32(smem + C::kOffP) + r * 128;
     const int c0 = gi * CG;  // first key column of this group
 
     double a_d = 0.0;      // running log remaining mass (natural log), f64
     float a2 = 0.0f;       // same in log2 units, f32, feeds the exponent
-    bool act[2] = {qb0 < g.nb, qb0 + 1 < g.nb};  // halves still sweeping
+    bool act[2] = {qb0 < u.nb, qb0 + 1 < u.nb};  // halves still sweeping
     int lowest = my_qb;    // leftmost processed key block (first_kb)
     int visited = 0;
     for (int j = 0; j < n_kv; ++j) {
@@ -342,8 +344,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
     }
     tmem_wait_ld();
     if (row_valid) {
-      __nv_bfloat16* orow =
-          args.o + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl + gi * DC;
+      __nv_bfloat16* orow = args.o + u.out_off + (int64_t)row * g.sl + gi * DC;
       uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
       for (int q4 = 0; q4 < DC / 8; ++q4)
@@ -351,10 +352,10 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
                              pack_bf16(ov[8 * q4 + 2], ov[8 * q4 + 3]),
                              pack_bf16(ov[8 * q4 + 4], ov[8 * q4 + 5]),
                              pack_bf16(ov[8 * q4 + 6], ov[8 * q4 + 7]));
-      if (gi == 0) args.log_rem[unit * g.L + row] = (float)a_d;
+      if (gi == 0) args.log_rem[u.rem_off + row * u.rem_stride] = (float)a_d;
     }
-    if (gi == 0 && my_qb < g.nb && (r & 63) == 0) {
-      args.first_kb[unit * g.nb + my_qb] = lowest;
+    if (gi == 0 && my_qb < u.nb && (r & 63) == 0) {
+      args.first_kb[u.fkb_off + my_qb] = lowest;
       if (args.counters) atomicAdd(args.counters, (unsigned long long)visited);
     }
   }

@@ -53,14 +53,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   // pair p covers query tiles 2p (WG0) and 2p+1 (WG1); heaviest pairs first
   // (longest-processing-time order keeps the tail short)
   const int BH = g.B * g.H;
-  const int n_pairs = (g.n_qt + 1) / 2;
   int item, bh;
-  grouped_order((int)blockIdx.x, n_pairs, BH, item, bh);
-  const int p = n_pairs - 1 - item;
+  grouped_order((int)blockIdx.x, (g.n_qt + 1) / 2, BH, item, bh);
   const int b = bh / g.H, h = bh % g.H;
-  const bool has1 = 2 * p + 1 < g.n_qt;
-  const int kbhi0 = min(4 * p + 1, g.nb - 1);
-  const int kbhi1 = has1 ? min(4 * p + 3, g.nb - 1) : kbhi0;
+  const Unit u = make_unit(g, b, h);
+  const int n_pairs = (u.n_qt + 1) / 2;
+  if (item >= n_pairs) return;  // shorter sequence of a varlen batch: no work
+  const int p = n_pairs - 1 - item;
+  const bool has1 = 2 * p + 1 < u.n_qt;
+  const int kbhi0 = min(4 * p + 1, u.nb - 1);
+  const int kbhi1 = has1 ? min(4 * p + 3, u.nb - 1) : kbhi0;
   const int n_s = kbhi1 + 1;  // stream tiles, kb = kbhi1 .. 0
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       for (int w = 0; w < (has1 ? 2 : 1); ++w)
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_q, bar_q, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128), c * 64,
-                      (2 * p + w) * kTileM, h, b);
+                      u.trow0 + (2 * p + w) * kTileM, h, u.tb);
       for (int j = 0; j < n_s; ++j) {
         const int s = j % ST;
         if (j >= ST) mbar_wait(bar_kvempty + s, ((j / ST) - 1) & 1);
@@ -114,11 +116,11 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         mbar_expect_tx(bar_kfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_k, bar_kfull + s, smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kb * kBlock, h, b);
+                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
         mbar_expect_tx(bar_vfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, kb * kBlock, h, b);
+                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
       }
     }
   } else if (warp == 9 || warp == 10) {
@@ -145,6 +147,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       auto issue_pv = [&](int i) {  // local tile i == stream tile j0 + i
         const int s = (j0 + i) % ST;
         mbar_wait(pfull + (i & 1), (i >> 1) & 1);
+        SB_TR(args, 2 + w, i, 9);
         mbar_wait(bar_vfull + s, ((j0 + i) / ST) & 1);
         tc_fence_after();
         if (leader) {
@@ -196,24 +199,27 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const int qt = 2 * p + w;
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
-      const bool row_valid = row < g.L;
+      const bool row_valid = row < u.L;
       const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
       const uint32_t tS = tbase + w * 128 + lane_base, tO = tbase + 256 + w * 128 + lane_base;
-      const int64_t unit = (int64_t)b * g.H + h;
-      float* Mrow = args.M + unit * g.n_tiles * kBlock + (r & 63);
+      float* Mrow = args.M + u.m_off + (r & 63);
       const uint32_t p_row = smem_u32(smem + C::kOffP + w * 2 * C::kPBytes) + r * 128;
       const int kbhi = w ? kbhi1 : kbhi0;
       const int n_w = kbhi + 1;
       const float sl2 = g.scale_log2;
       float a2 = 0.0f;  // running log2 remaining mass
+      const bool tr = quarter == 0 && lane == 0;
+      if (tr) SB_TR(args, w, 0, 14);
       for (int i = 0; i < n_w; ++i) {
         const int kb = kbhi - i;
+        if (tr) SB_TR(args, w, i, 0);
         mbar_wait(sfull + (i & 1), (i >> 1) & 1);
         tc_fence_after();
         float s[64];
         tmem_ld32(tS + (i & 1) * 64, s);
         tmem_ld32(tS + (i & 1) * 64 + 32, s + 32);
         tmem_wait_ld();
+        if (tr) SB_TR(args, w, i, 1);
         uint32_t pk[32];
         bool slow = false;
         const bool diag = kb == my_qb;
@@ -260,7 +266,9 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(sempty + (i & 1));
+        if (tr) SB_TR(args, w, i, 2);
         if (i >= 2) mbar_wait(pempty + (i & 1), ((i >> 1) + 1) & 1);
+        if (tr) SB_TR(args, w, i, 3);
         const uint32_t pb = p_row + (i & 1) * C::kPBytes;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
@@ -268,11 +276,12 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
                        pk[4 * c + 3]);
         fence_proxy_async_smem();
         mbar_arrive(pfull + (i & 1));
+        if (tr) SB_TR(args, w, i, 4);
       }
       // epilogue
       mbar_wait(bar_ofull + w, 0);
       tc_fence_after();
-      __nv_bfloat16* orow = args.o + (int64_t)b * g.sb + (int64_t)h * g.sh + (int64_t)row * g.sl;
+      __nv_bfloat16* orow = args.o + u.out_off + (int64_t)row * g.sl;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         float ov[32];
@@ -288,9 +297,9 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
                                  pack_bf16(ov[8 * q4 + 6], ov[8 * q4 + 7]));
         }
       }
-      if (row_valid) args.log_rem[unit * g.L + row] = a2 * kLn2;
-      if (my_qb < g.nb && (r & 63) == 0) {
-        args.first_kb[unit * g.nb + my_qb] = 0;
+      if (row_valid) args.log_rem[u.rem_off + row * u.rem_stride] = a2 * kLn2;
+      if (my_qb < u.nb && (r & 63) == 0) {
+        args.first_kb[u.fkb_off + my_qb] = 0;
         if (args.counters) atomicAdd(args.counters, (unsigned long long)(my_qb + 1));
       }
     }

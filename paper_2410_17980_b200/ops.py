@@ -17,8 +17,12 @@ reference                          this module
 
 Tensors are CUDA bf16 of shape (B, H, L, d) (any strides with a contiguous last
 dim; q, k, v share one layout).  Unlike the reference (one L x d head per call)
-every call covers all (batch, head) units at once.  Errors the reference raises
-as ValueError are raised as ValueError here.  There is no CPU fallback.
+every call covers all (batch, head) units at once.  Packed variable-length
+batches pass (total_tokens, H, d) tensors with
+``cu_seqlens`` (int32 [n_seq+1] offsets): every sequence is planned and run as
+an independent problem, exactly as the reference runs each sequence separately.
+Errors the reference raises as ValueError are raised as ValueError here.  There
+is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -95,6 +99,8 @@ class BlockedCache:
     M: torch.Tensor
     skip: bool
     skip_eps: float
+    cu_seqlens: torch.Tensor | None = None  # varlen: device int32 [n_seq+1]
+    max_seqlen: int = 0
 
 
 def _ptr(t):
@@ -105,10 +111,12 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _check_qkv(q, k, v):
+def _check_qkv(q, k, v, varlen=False):
     if not (q.shape == k.shape == v.shape):
         raise ValueError("q, k, v must share one shape")  # blocked.py:116-117
-    if q.dim() != 4:
+    if varlen and q.dim() != 3:
+        raise ValueError("varlen q, k, v must be (total_tokens, heads, head_dim)")
+    if not varlen and q.dim() != 4:
         raise ValueError("q, k, v must be (batch, heads, seq_len, head_dim)")
     for t in (q, k, v):
         if not t.is_cuda:
@@ -131,13 +139,23 @@ def _same_layout(*ts):
     return out
 
 
-def _params(q, scale, skip, skip_eps, block=DEFAULT_BLOCK) -> _lib.SbParams:
-    B, H, L, d = q.shape
-    sb, sh, sl, sd = q.stride()
+def _params(q, scale, skip, skip_eps, block=DEFAULT_BLOCK, cu_seqlens=None,
+            max_seqlen=0) -> _lib.SbParams:
     p = _lib.SbParams()
-    p.batch, p.heads, p.seqlen, p.head_dim = B, H, L, d
-    p.stride_b, p.stride_h, p.stride_l = sb, sh, sl
-    p.cu_seqlens = None
+    if cu_seqlens is None:
+        B, H, L, d = q.shape
+        sb, sh, sl, sd = q.stride()
+        p.batch, p.heads, p.seqlen, p.head_dim = B, H, L, d
+        p.stride_b, p.stride_h, p.stride_l = sb, sh, sl
+        p.cu_seqlens = None
+        p.total_tokens = 0
+    else:
+        T, H, d = q.shape
+        sl, sh, sd = q.stride()
+        p.batch, p.heads, p.seqlen, p.head_dim = cu_seqlens.numel() - 1, H, max(1, max_seqlen), d
+        p.stride_b, p.stride_h, p.stride_l = 0, sh, sl
+        p.cu_seqlens = ctypes.c_void_p(cu_seqlens.data_ptr())
+        p.total_tokens = T
     p.scale = float(scale)
     p.block = block
     p.skip = int(bool(skip))
@@ -145,14 +163,70 @@ def _params(q, scale, skip, skip_eps, block=DEFAULT_BLOCK) -> _lib.SbParams:
     return p
 
 
+def _varlen_plan(cu_seqlens, q):
+    """Host copy of the offsets (one small D2H read) -> (lengths, max_seqlen)."""
+    if cu_seqlens.dtype != torch.int32 or cu_seqlens.dim() != 1 or cu_seqlens.numel() < 2:
+        raise ValueError("cu_seqlens must be a 1-D int32 tensor of n_seq+1 offsets")
+    host = cu_seqlens.cpu()
+    lens = (host[1:] - host[:-1]).tolist()
+    if host[0].item() != 0 or min(lens) < 0 or host[-1].item() != q.shape[0]:
+        raise ValueError("cu_seqlens must start at 0, be non-decreasing and end at total_tokens")
+    return host, lens, max(lens)
+
+
+def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters):
+    _check_qkv(q, k, v, varlen=True)
+    T, H, d = q.shape
+    host, lens, max_L = _varlen_plan(cu_seqlens, q)
+    if skip_eps is None:
+        skip_eps = default_skip_eps(q.dtype)
+    if not 0.0 < skip_eps < 1.0:
+        raise ValueError("skip_eps must be in (0, 1)")  # blocked.py:155-156
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    q, k, v = _same_layout(q, k, v)
+    cu = cu_seqlens.to(device=q.device, dtype=torch.int32).contiguous()
+    lib = _lib.load()
+    p = _params(q, scale, skip, skip_eps, cu_seqlens=cu, max_seqlen=max_L)
+    n_snap, n_fkb = ctypes.c_size_t(), ctypes.c_size_t()
+    host_c = host.to(torch.int32).contiguous()
+    _lib.check(lib.sb_varlen_elems(ctypes.byref(p), ctypes.c_void_p(host_c.data_ptr()),
+                                   ctypes.byref(n_snap), ctypes.byref(n_fkb)))
+    o = torch.empty_like(q)
+    log_rem = torch.empty((T, H), device=q.device, dtype=torch.float32)
+    first_kb = torch.empty(max(1, n_fkb.value), device=q.device, dtype=torch.int32)
+    M = torch.empty(max(1, n_snap.value), device=q.device, dtype=torch.float32)
+    cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
+    if max_L > 0:
+        _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
+                              _ptr(first_kb), _ptr(M), _ptr(cnt), _stream()))
+    else:
+        o.zero_()
+        log_rem.zero_()
+    total = n_snap.value // DEFAULT_BLOCK
+    visited = int(cnt[0].item()) if counters else -1
+    stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
+    cache = BlockedCache(q, k, v, scale, None, log_rem, first_kb, M, skip, skip_eps,
+                         cu_seqlens=cu, max_seqlen=max_L)
+    return o, log_rem, stats, cache
+
+
 def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = False,
                     skip_eps: float | None = None, scale: float | None = None,
-                    counters: bool = True):
+                    counters: bool = True, cu_seqlens: torch.Tensor | None = None):
     """blocked_forward(two_phase=True) over every (b, h) unit (blocked.py:129-206).
 
     Returns (o, log_rem, TileStats, BlockedCache).  log_rem is the reference's
     RowLogAccumulator.a (natural log of the remaining stick mass).
+
+    Varlen: q, k, v (total_tokens, H, d) with cu_seqlens (int32 [n_seq+1]);
+    log_rem is then (total_tokens, H), first_kb a flat array packed sequence by
+    sequence (head-major within a sequence), layout must be None.
     """
+    if cu_seqlens is not None:
+        if layout is not None:
+            raise ValueError("varlen batches are planned per sequence; pass layout=None")
+        return _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters)
     _check_qkv(q, k, v)
     B, H, L, d = q.shape
     if layout is None:
@@ -198,7 +272,7 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     subtracted from dO.V^T per query row (blocked.py:241-242).
     """
     if layout is not None and layout != cache.layout:
-        raise ValueError("layout does not match the one the cache was built with")
+        raise ValueError("layout does not match the one the cache was built with")  # :398-399
     if cache.M is None:
         raise ValueError("two-phase backward needs a forward run with two_phase=True "
                          "(M snapshots missing)")
@@ -210,7 +284,8 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     if d_o.stride() != q.stride() or d_o.data_ptr() % 16:
         d_o = torch.empty_like(q).copy_(d_o)
     lib = _lib.load()
-    p = _params(q, cache.scale, cache.skip, cache.skip_eps)
+    p = _params(q, cache.scale, cache.skip, cache.skip_eps, cu_seqlens=cache.cu_seqlens,
+                max_seqlen=cache.max_seqlen)
     if out is None:  # (N, dq, dk, dv); callers running the phases one by one pass it
         out = (torch.empty_like(cache.M), torch.empty_like(q), torch.empty_like(q),
                torch.empty_like(q))
@@ -219,18 +294,23 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     if row_offset is not None:
         ro = row_offset.to(device=q.device, dtype=torch.float32).contiguous()
         if ro.shape != cache.log_rem.shape:
-            raise ValueError("row_offset must be (batch, heads, seq_len)")
+            raise ValueError("row_offset must match log_rem: (batch, heads, seq_len), or "
+                             "(total_tokens, heads) for varlen")
+    if cache.cu_seqlens is not None and cache.max_seqlen == 0:
+        return dq.zero_(), dk.zero_(), dv.zero_(), 0
     _lib.check(lib.sb_bwd_phase(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
                                 _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M),
                                 _ptr(N), _ptr(dq), _ptr(dk), _ptr(dv), int(phases), _stream()))
-    return dq, dk, dv, cache.layout.n_tiles * q.shape[0] * q.shape[1]
+    n_stored = (cache.M.numel() // DEFAULT_BLOCK if cache.cu_seqlens is not None
+                else cache.layout.n_tiles * q.shape[0] * q.shape[1])
+    return dq, dk, dv, n_stored
 
 
 class _StickBreakingFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, scale, skip, skip_eps):
+    def forward(ctx, q, k, v, scale, skip, skip_eps, cu_seqlens):
         o, log_rem, _, cache = blocked_forward(q, k, v, skip=skip, skip_eps=skip_eps,
-                                               scale=scale, counters=False)
+                                               scale=scale, counters=False, cu_seqlens=cu_seqlens)
         ctx.cache = cache
         ctx.save_for_backward(cache.q, cache.k, cache.v, cache.log_rem, cache.first_kb, cache.M)
         rem = torch.exp(log_rem)
@@ -241,18 +321,20 @@ class _StickBreakingFn(torch.autograd.Function):
     def backward(ctx, d_o, d_rem):
         q, k, v, log_rem, first_kb, M = ctx.saved_tensors
         c = ctx.cache
-        cache = BlockedCache(q, k, v, c.scale, c.layout, log_rem, first_kb, M, c.skip, c.skip_eps)
+        cache = BlockedCache(q, k, v, c.scale, c.layout, log_rem, first_kb, M, c.skip, c.skip_eps,
+                             cu_seqlens=c.cu_seqlens, max_seqlen=c.max_seqlen)
         if d_o is None:
             d_o = torch.zeros_like(q)
         # rem_j = 1 - sum_i A_ij  =>  dL/dA_ij -= dL/drem_j : the reference's
         # row_offset hook (blocked.py:241-242, model.py:227-230)
         dq, dk, dv, _ = blocked_backward_twophase(cache, d_o.to(torch.bfloat16), row_offset=d_rem)
-        return dq, dk, dv, None, None, None
+        return dq, dk, dv, None, None, None, None
 
 
 def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool = False,
                             skip_eps: float | None = None, return_rem: bool = False,
-                            attend_current: bool = False):
+                            attend_current: bool = False,
+                            cu_seqlens: torch.Tensor | None = None):
     """Stick-breaking attention (arXiv 2410.17980), strictly causal.
 
     q, k, v: CUDA bf16 (batch, heads, seq_len, head_dim), head_dim 64 or 128.
@@ -261,14 +343,17 @@ def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool =
     remaining stick mass rem_j = 1 - sum_i A_ij (B, H, L) float32 is returned too
     and is differentiable.  skip enables the reference's block skipping
     (exact: a skipped block's weights are below skip_eps).
+
+    Packed varlen: q, k, v (total_tokens, heads, head_dim) and cu_seqlens (int32
+    [n_seq+1] offsets); each sequence attends only within itself.
     """
     if attend_current:
         raise ValueError("attend_current=True is not part of the reference semantics "
                          "(strict causality, attention.py:52-54)")
-    _check_qkv(q, k, v)
+    _check_qkv(q, k, v, varlen=cu_seqlens is not None)
     if skip_eps is None:
         skip_eps = SKIP_EPS_BF16
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[-1])
-    o, rem = _StickBreakingFn.apply(q, k, v, float(scale), bool(skip), float(skip_eps))
+    o, rem = _StickBreakingFn.apply(q, k, v, float(scale), bool(skip), float(skip_eps), cu_seqlens)
     return (o, rem) if return_rem else o

@@ -1,0 +1,104 @@
+"""Packed variable-length batches (cu_seqlens) on the GPU.
+
+The reference has no varlen entry point: its semantics for a batch of sequences
+is one independent blocked_forward / blocked_backward_twophase run per sequence
+(blocks aligned to every sequence start).  So the packed result for sequence b
+must equal, bit for bit, the uniform-batch result of that sequence alone, and
+match the CPU oracle run on that sequence (bf16 tolerance 2e-2, skip decisions
+bit-exact).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import oracle_bwd, oracle_fwd, rel_to_max, to64
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def packed(lens, H, d, seed, family="random", mu=-6.0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    T = sum(lens)
+    ts = [torch.randn(T, H, d, generator=g) for _ in range(4)]
+    if family == "shift":
+        ts[0][..., 0] = mu * d ** 0.5
+        ts[1][..., 0] = 1.0
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    return [t.to(torch.bfloat16).cuda() for t in ts], cu.cuda()
+
+
+def seq(t, cu, b):
+    """(L_b, H, d) slice of a packed tensor as a (1, H, L_b, d) uniform batch."""
+    s0, s1 = int(cu[b]), int(cu[b + 1])
+    return t[s0:s1].transpose(0, 1).unsqueeze(0).contiguous()
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_varlen_equals_per_sequence_runs(d):
+    import paper_2410_17980_b200 as sb
+    lens = [100, 0, 257, 64, 1, 513, 130]
+    H = 2
+    (q, k, v, d_o), cu = packed(lens, H, d, seed=d)
+    o, log_rem, st, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu)
+    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o)
+    torch.cuda.synchronize()
+    assert st.visited == st.total == H * sum((n + 63) // 64 * ((n + 63) // 64 + 1) // 2
+                                             for n in lens)
+    for b, L in enumerate(lens):
+        if L == 0:
+            continue
+        qs, ks, vs, ds = (seq(t, cu, b) for t in (q, k, v, d_o))
+        o1, lr1, _, c1 = sb.blocked_forward(qs, ks, vs)
+        dq1, dk1, dv1, _ = sb.blocked_backward_twophase(c1, ds)
+        s0, s1 = int(cu[b]), int(cu[b + 1])
+        assert torch.equal(seq(o, cu, b), o1), b
+        assert torch.equal(log_rem[s0:s1].transpose(0, 1).unsqueeze(0), lr1), b
+        for got, ref in ((dq, dq1), (dk, dk1), (dv, dv1)):
+            assert torch.equal(seq(got, cu, b), ref), b
+
+
+def test_varlen_matches_oracle_and_autograd():
+    import paper_2410_17980_b200 as sb
+    lens = [300, 77, 192]
+    H, d = 2, 64
+    (q, k, v, d_o), cu = packed(lens, H, d, seed=5)
+    qq, kk, vv = (t.clone().requires_grad_(True) for t in (q, k, v))
+    o, rem = sb.stickbreaking_attention(qq, kk, vv, cu_seqlens=cu, return_rem=True)
+    o.backward(d_o)
+    torch.cuda.synchronize()
+    assert rem.shape == (sum(lens), H)
+    for b in range(len(lens)):
+        qs, ks, vs, ds = (seq(t, cu, b)[0] for t in (q, k, v, d_o))
+        ref = oracle_fwd(qs, ks, vs)
+        rdq, rdk, rdv, _ = oracle_bwd(qs, ks, vs, ds, ref)
+        assert rel_to_max(to64(seq(o.detach(), cu, b)[0]), ref["o"]) < TOL
+        for got, r in ((qq.grad, rdq), (kk.grad, rdk), (vv.grad, rdv)):
+            assert rel_to_max(to64(seq(got, cu, b)[0]), r) < TOL
+
+
+def test_varlen_skip_decisions_bit_exact():
+    import paper_2410_17980_b200 as sb
+    lens = [1024, 300, 640]
+    H, d = 2, 128
+    (q, k, v, _), cu = packed(lens, H, d, seed=3, family="shift", mu=-6.0)
+    o, log_rem, st, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu, skip=True, skip_eps=1e-6)
+    torch.cuda.synchronize()
+    fkb = st.first_kb.cpu().numpy()
+    off = 0
+    visited = 0
+    for b, L in enumerate(lens):
+        nb = (L + 63) // 64
+        qs, ks, vs = (seq(t, cu, b)[0] for t in (q, k, v))
+        ref = oracle_fwd(qs, ks, vs, skip=True, skip_eps=1e-6)
+        np.testing.assert_array_equal(fkb[off:off + H * nb].reshape(H, nb), ref["first_kb"])
+        off += H * nb
+        visited += ref["visited"]
+    assert st.visited == visited

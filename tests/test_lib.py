@@ -78,6 +78,37 @@ def test_invalid_arguments_rejected_before_launch(lib, kw, code):
     assert rc == code
 
 
+def test_varlen_elems(lib):
+    """Packed varlen: each sequence is planned separately (blocked.py:63-67 per sequence)."""
+    p = _params(B=3, H=2, L=200)
+    cu = (ctypes.c_int32 * 4)(0, 200, 200, 265)  # lengths 200, 0, 65
+    snap, fkb = ctypes.c_size_t(), ctypes.c_size_t()
+    assert lib.sb_varlen_elems(ctypes.byref(p), cu, ctypes.byref(snap), ctypes.byref(fkb)) == 0
+    nbs = [4, 0, 2]
+    assert snap.value == 2 * sum(n * (n + 1) // 2 for n in nbs) * 64
+    assert fkb.value == 2 * sum(nbs)
+    bad = (ctypes.c_int32 * 4)(0, 200, 100, 265)
+    assert lib.sb_varlen_elems(ctypes.byref(p), bad, ctypes.byref(snap), ctypes.byref(fkb)) == 1
+
+
+def test_varlen_needs_total_tokens(lib):
+    p = _params(B=2, H=2, L=128)
+    cu = (ctypes.c_int32 * 3)(0, 64, 128)
+    p.cu_seqlens = ctypes.cast(cu, ctypes.c_void_p)
+    p.total_tokens = 0
+    d = ctypes.c_void_p(16)
+    assert lib.sb_fwd(ctypes.byref(p), d, d, d, d, d, d, d, None, None) == 1
+
+
+def test_python_varlen_validation():
+    import torch
+    import paper_2410_17980_b200 as sb
+    q = torch.zeros(10, 2, 64, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):  # 4-D tensors are not a packed batch
+        sb.stickbreaking_attention(q[None], q[None], q[None],
+                                   cu_seqlens=torch.tensor([0, 10], dtype=torch.int32))
+
+
 def test_missing_snapshots_rejected(lib):
     """blocked.py:315-316: two-phase backward without M snapshots is an error."""
     p = _params()

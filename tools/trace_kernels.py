@@ -45,14 +45,19 @@ def main():
     for it in range(3):  # warm, then traced
         if it == 2:
             lib.sb_debug_set_trace(tr.data_ptr())
-        ops.blocked_backward_twophase(cache, do)
+        if a.phase == 0:  # forward
+            ops.sb_forward_blocked(q, k, v)
+        elif a.phase == 2:
+            ops.blocked_backward_twophase(cache, do)
+        else:  # phase 1 only, traced
+            ops.blocked_backward_twophase(cache, do, phases=1)
         torch.cuda.synchronize()
     lib.sb_debug_set_trace(None)
     t = tr.cpu().numpy().view(np.uint32).reshape(NCTA, NROLE, NT, NEV).astype(np.int64)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     np.save(os.path.join(ROOT, "gpurun_out", f"trace_p{a.phase}.npy"), t)
     for c in range(NCTA):
-        base = t[c, 0, 0, 14]
+        base = t[c, 0, 0, 14] if t[c, 0, 0, 14] else t[c, 1, 0, 14]
         print(f"CTA {c}: start->done {t[c, 0, 0, 15] - base} clk")
         for role in range(NROLE):
             rows = []
