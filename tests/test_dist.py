@@ -56,3 +56,67 @@ def test_two_rank_shard_and_gather_bit_identical(tmp_path):
                                           block=64, n_threads=1)
     for name, ref in (("o", fwd["o"]), ("dq", dq), ("dk", dk), ("dv", dv)):
         assert np.array_equal(got[name].numpy(), ref), name
+
+
+def test_lpt_assign_balances_quadratic_cost():
+    lens = [8192, 512, 4096, 4096, 2048, 1024, 8192, 512]
+    a = sbdist.lpt_assign(lens, 2)
+    assert sorted(sum(a, [])) == list(range(len(lens)))
+    loads = [sum(lens[i] ** 2 for i in s) for s in a]
+    assert max(loads) / min(loads) < 1.1
+    assert sbdist.lpt_assign(lens, 1) == [list(range(len(lens)))]
+
+
+def _varlen_worker(rank, world, port, q, k, v, cu, lens, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    assign = sbdist.lpt_assign(lens, world)
+    qs, ks, vs = (sbdist.shard_varlen(t, cu, assign[rank])[0] for t in (q, k, v))
+    _, cul = sbdist.shard_varlen(q, cu, assign[rank])
+    o = torch.zeros_like(qs)
+    for i in range(len(assign[rank])):  # per-sequence oracle stands in for the kernel
+        s0, s1 = int(cul[i]), int(cul[i + 1])
+        f = oracle.tiled_forward(qs[s0:s1].transpose(0, 1).numpy(), ks[s0:s1].transpose(0, 1).numpy(),
+                                 vs[s0:s1].transpose(0, 1).numpy(), block=64, n_threads=1)
+        o[s0:s1] = torch.from_numpy(f["o"]).transpose(0, 1)
+    full = sbdist.gather_varlen(o, cu, assign)
+    if rank == 0:
+        torch.save(full, os.path.join(out_dir, "varlen.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_varlen_lpt_shard_and_gather_bit_identical(tmp_path):
+    g = torch.Generator().manual_seed(1)
+    lens = [70, 130, 20, 64]
+    H, d = 2, 16
+    T = sum(lens)
+    q, k, v = (torch.randn(T, H, d, generator=g, dtype=torch.float64) for _ in range(3))
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    mp.spawn(_varlen_worker, args=(2, _free_port(), q, k, v, cu, lens, str(tmp_path)), nprocs=2,
+             join=True)
+    got = torch.load(os.path.join(tmp_path, "varlen.pt"))
+    for i, L in enumerate(lens):
+        s0 = int(cu[i])
+        f = oracle.tiled_forward(q[s0:s0 + L].transpose(0, 1).numpy(),
+                                 k[s0:s0 + L].transpose(0, 1).numpy(),
+                                 v[s0:s0 + L].transpose(0, 1).numpy(), block=64, n_threads=1)
+        assert np.array_equal(got[s0:s0 + L].transpose(0, 1).numpy(), f["o"]), i
+
+
+def test_lpt_units_split_heads_when_sequences_are_too_coarse():
+    lens = [7045, 5404, 4438, 2584, 2876, 826, 1089, 638, 1858, 6758, 5500, 7522, 4380, 5171,
+            7968, 1479]
+    G, a = sbdist.lpt_assign_units(lens, 16, 8)
+    units = sorted(sum(a, []))
+    assert units == sorted((i, g) for i in range(len(lens)) for g in range(G))
+    loads = [sum(lens[i] ** 2 for i, _ in s) for s in a]
+    assert max(loads) / (sum(loads) / 8) <= 1.05
+    assert G > 1  # whole sequences alone cannot balance 8 ranks here
+    x = torch.arange(sum(lens) * 16 * 2, dtype=torch.float32).reshape(sum(lens), 16, 2)
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    t, c = sbdist.shard_varlen_units(x, cu, a[0], G)
+    assert t.shape[1] == 16 // G and int(c[-1]) == t.shape[0] and c.numel() == len(a[0]) + 1
+    i, g = a[0][0]
+    hg = 16 // G
+    assert torch.equal(t[: lens[i]], x[int(cu[i]): int(cu[i]) + lens[i], g * hg:(g + 1) * hg])
