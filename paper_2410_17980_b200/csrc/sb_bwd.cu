@@ -106,12 +106,12 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
 template <bool kOff>
 __device__ __forceinline__ void load_dat(float* s, uint32_t taddr, float off) {
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    float w[16];
-    tmem_ld16(taddr + ch * 16, w);
+  for (int ch = 0; ch < 2; ++ch) {
+    float w[32];
+    tmem_ld32(taddr + ch * 32, w);
     tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < 16; ++c) s[ch * 16 + c] *= kOff ? (w[c] - off) : w[c];
+    for (int c = 0; c < 32; ++c) s[ch * 32 + c] *= kOff ? (w[c] - off) : w[c];
   }
 }
 

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           umma_commit(bar_kvempty + s);
         }
         __syncwarp();
+        SB_TR(args, 2 + w, i, 11);
       };
       for (int j = 0; j < j0; ++j) {  // stream tiles right of this WG's diagonal
         mbar_wait(bar_vfull + j % ST, (j / ST) & 1);
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         const int j = j0 + i, s = j % ST;
         mbar_wait(bar_kfull + s, (j / ST) & 1);
         if (i >= 2) mbar_wait(sempty + (i & 1), ((i >> 1) + 1) & 1);
+        SB_TR(args, 2 + w, i, 8);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           umma_commit(sfull + (i & 1));
         }
         __syncwarp();
+        SB_TR(args, 2 + w, i, 10);
         if (i >= 1) issue_pv(i - 1);
       }
       issue_pv(n_w - 1);
