@@ -8,8 +8,8 @@
 //   b carried in registers, N snapshot = b in effect per tile, dQ += dZ K.
 // Phase 2 (:367-386): per 64-key block, query tiles top to bottom over visited
 //   tiles, b = N snapshot, dK += dZ^T Q, dV += A^T dO — owned rows, no atomics,
-//   deterministic.  dK^T and dV^T are accumulated in TMEM with M = head_dim
-//   (A^T / dZ^T reach the tensor core through MN-major smem descriptors).
+//   deterministic.  dK and dV are accumulated in TMEM with M = 128 keys (A^T /
+//   dZ^T reach the tensor core through MN-major smem descriptors).
 //
 // Both phases use the ping-pong layout of sb_fwd_pp.cu: two stick warpgroups
 // per CTA (thread r <-> TMEM lane r <-> query row, all 64 key columns of a tile
@@ -17,7 +17,8 @@
 //   phase 1: WG w owns query tile 2p+w; both share one K/V stream.
 //   phase 2: WG w owns key block 2p+w; both share one Q/dO stream.
 // Tile math is the product form (sb_common.cuh): A_c = sigma_c * e^M *
-// prod_{c'>c} r_c', sigma = t/(1+t), r = 1/(1+t): one ex2 + one rcp per element.
+// prod_{c'>c} r_c', sigma = t/(1+t), r = 1/(1+t), with one rcp per 16 columns
+// (batched reciprocal, recompute_row).
 // Warps: 0-3 WG0, 4-7 WG1, 8 TMA producer (+TMEM allocator), 9/10 MMA for WG0/WG1,
 // 11 idle; warpgroup 2 hands its registers to the stick warpgroups (setmaxnreg).
 #include "sb_args.cuh"
@@ -423,21 +424,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (tr) SB_TR(args, w, 0, 15);
       tc_fence_after();
       const float scale = g.scale_log2 * kLn2;
-      __nv_bfloat16* dqrow = args.dq + u.out_off + (int64_t)row * g.sl;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        float v[32];
-        tmem_ld32(tQ + c * 32, v);
+      // dQ rows leave in 64-column halves through this warp's 4 KB slice of the
+      // (now idle: `done`) dZ buffer as coalesced row segments
+      const int row0 = qt * kTileM + quarter * 32;
+      const int nvalid = max(0, min(32, u.L - row0));
+      const uint32_t stage = smem_u32(smem + C::kOffZ + w * C::kZBytes) + quarter * 4096;
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        float v[64];
+        tmem_ld32(tQ + c * 64, v);
+        tmem_ld32(tQ + c * 64 + 32, v + 32);
         tmem_wait_ld();
-        if (row_valid) {
-          uint4* dst = reinterpret_cast<uint4*>(dqrow + c * 32);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            dst[q4] = make_uint4(pack_bf16(v[8 * q4] * scale, v[8 * q4 + 1] * scale),
-                                 pack_bf16(v[8 * q4 + 2] * scale, v[8 * q4 + 3] * scale),
-                                 pack_bf16(v[8 * q4 + 4] * scale, v[8 * q4 + 5] * scale),
-                                 pack_bf16(v[8 * q4 + 6] * scale, v[8 * q4 + 7] * scale));
-        }
+        warp_store_rows<8>(v, scale, stage, args.dq + u.out_off + (int64_t)row0 * g.sl + c * 64,
+                           g.sl, nvalid);
       }
     }
   }
@@ -448,16 +447,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 // ============================================================================
 // Phase 2: dK and dV.  CTA = (b, h, key blocks 2p and 2p+1 = one 128-key pair);
-// query tiles stream top to bottom.  Warpgroup w owns key block 2p+w (thread r
-// <-> query row r of the tile for the stick math, <-> head-dim index r for the
-// dK^T/dV^T epilogue).  Every MMA spans BOTH key blocks (N = 128 keys): the
+// query tiles stream top to bottom.  Warpgroup w owns key block 2p+w for the
+// stick math (thread r <-> query row r of the tile) and head-dim half w of the
+// dK/dV epilogue (thread r <-> key r of the pair).  Every MMA spans BOTH key blocks (N = 128 keys): the
 // tensor core's shared-memory operand traffic per FLOP is 2/3 of two N = 64 MMAs
 // (measured: 128x64x16 SS-MMAs are smem-bound at 48 clk, 128x128x16 run at the
 // full 64 clk), and one elected thread issues everything in a fixed order.
-//   S    = Q  [K0;K1]^T   (M=128 rows, N=128 keys)  TMEM cols   0..127
-//   dW   = dO [V0;V1]^T                             TMEM cols 128..255
-//   dV^T += dO^T [A0 A1]  (M=D, N=128 keys, K=128 rows)  cols 256..383
-//   dK^T += Q^T [dZ0 dZ1]                                cols 384..511
+//   S   = Q  [K0;K1]^T    (M=128 rows, N=128 keys)       TMEM cols   0..127
+//   dW  = dO [V0;V1]^T                                    TMEM cols 128..255
+//   dV += [A0 A1]^T dO    (M=128 keys, N=D, K=128 rows)   cols 256..256+D
+//   dK += [dZ0 dZ1]^T Q                                   cols 384..384+D
+// dV/dK come out key-major (lane = key), so the epilogue writes whole key rows.
 template <int D>
 struct BwdKVCfg {
   static constexpr int kStages = D == 128 ? 2 : 3;
@@ -469,7 +469,7 @@ struct BwdKVCfg {
   static constexpr int kOffQ = kOffV + kPairBytes;               // stage s: Q, dO
   static constexpr int kOffAZ = kOffQ + kStages * 2 * kQBytes;   // WG0 then WG1 (contiguous)
   static constexpr int kOffBar = kOffAZ + 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 9;
+  static constexpr int kNumBars = 1 + 2 * kStages + 11;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
@@ -516,6 +516,32 @@ struct LiveQt {
   }
 };
 
+// Work item of phase 2: (unit, key pair p).  Every role derives the same item
+// list, so they agree on which items carry work without communicating.
+struct KVItem {
+  Unit u;
+  int b, h, kb0;
+  bool valid;  // the key pair exists (varlen: shorter sequences have fewer)
+};
+__device__ __forceinline__ KVItem kv_item(const Geom& g, int idx) {
+  KVItem it;
+  int p, bh;
+  grouped_order(idx, (g.nb + 1) / 2, g.B * g.H, p, bh);
+  it.b = bh / g.H;
+  it.h = bh % g.H;
+  it.u = make_unit(g, it.b, it.h);
+  it.kb0 = 2 * p;
+  it.valid = it.kb0 < it.u.nb;
+  return it;
+}
+
+// Persistent: one CTA per SM walks the items idx = blockIdx.x, +gridDim.x, ...
+// (LPT order within groups of 8 units).  The Q/dO ring and every per-tile
+// barrier run on a CTA-wide tile counter across items, so the producer fetches
+// the next item's K/V and first Q/dO tiles while the warpgroups finish the
+// current item and write its dK/dV.  Per item: bar_kv (K/V landed), kv_free
+// (last S/dW of the item read K/V), done (last dK^T issued), acc_free (the
+// warpgroups read dV/dK out of TMEM).
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     sb_bwd_kv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -528,20 +554,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                              ~uintptr_t(1023));
   const Geom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // small key blocks first: they own the longest columns (LPT order)
-  const int BH = g.B * g.H;
-  int p, bh;
-  grouped_order((int)blockIdx.x, (g.nb + 1) / 2, BH, p, bh);
-  const int b = bh / g.H, h = bh % g.H;
-  const Unit u = make_unit(g, b, h);
-  if (2 * p >= u.nb) return;  // shorter sequence of a varlen batch: no work
-  const int kb0 = 2 * p;
-  const int* fkb = args.first_kb + u.fkb_off;
-  // stick warps: half = which 64-row half of the query tile, kb = own key block
-  LiveQt it{fkb, u.nb, u.n_qt, kb0, (warp & 3) >> 1, kb0 + ((warp >> 2) & 1), 0, 0u, 0u};
-  it.fill(p);  // query tile p holds the diagonal of key block 2p
-  const int qt_first = it.next();
-  const bool any = qt_first < u.n_qt;
+  const int n_items = ((g.nb + 1) / 2) * g.B * g.H;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* bar_kv = bars;
@@ -552,10 +565,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* wfull = sfull + 2;        // dW = dO V^T landed
   uint64_t* wempty = sfull + 3;       // dW read
   uint64_t* afull = sfull + 4;        // A of both warpgroups in smem
-  uint64_t* aused = sfull + 5;        // dV^T MMA read A
+  uint64_t* aused = sfull + 5;        // dV MMA read A
   uint64_t* zfull = sfull + 6;        // dZ in smem
   uint64_t* zused = sfull + 7;        // dK^T MMA read dZ
-  uint64_t* done = sfull + 8;
+  uint64_t* done = sfull + 8;         // item's last dK^T complete
+  uint64_t* kv_free = sfull + 9;      // item's last S / dW read K/V
+  uint64_t* acc_free = sfull + 10;    // dV/dK read out of TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   if (threadIdx.x == 0) {
@@ -573,6 +588,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(zfull, 256);
     mbar_init(zused, 1);
     mbar_init(done, 1);
+    mbar_init(kv_free, 1);
+    mbar_init(acc_free, 256);
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -584,7 +601,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp >= 8) {
     reg_dealloc<kRegsLowKV>();
-    if (warp == 8 && any) {
+    if (warp == 8) {
       // ---------------------------------------------------------- TMA producer
       const bool leader = elect_one();
       if (leader) {
@@ -592,56 +609,70 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_prefetch(&tm_do);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
-        // both key blocks; rows past L (odd nb) are zero-filled by the TMA
-        mbar_expect_tx(bar_kv, 2 * C::kPairBytes);
-        for (int w = 0; w < 2; ++w)  // the K/V tensor maps have 64-row boxes
-          for (int c = 0; c < D / 64; ++c) {
-            const int off = c * (2 * kBlock * 128) + w * (kBlock * 128);
-            tma_load_4d(&tm_k, bar_kv, smem + C::kOffK + off, c * 64,
-                        u.trow0 + (kb0 + w) * kBlock, h, u.tb);
-            tma_load_4d(&tm_v, bar_kv, smem + C::kOffV + off, c * 64,
-                        u.trow0 + (kb0 + w) * kBlock, h, u.tb);
-          }
       }
-      for (int j = 0, qt = qt_first; qt < u.n_qt; qt = it.next(), ++j) {
-        const int s = j % ST;
-        if (j >= ST) mbar_wait(bar_qempty + s, ((j / ST) - 1) & 1);
-        SB_TR(args, 2, j, 12);
+      int jg = 0, ni = 0;  // tiles and work items so far
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const KVItem wi = kv_item(g, idx);
+        if (!wi.valid) continue;
+        const Unit& u = wi.u;
+        LiveQt it{args.first_kb + u.fkb_off, u.nb, u.n_qt, wi.kb0, 0, wi.kb0, 0, 0u, 0u};
+        it.fill(wi.kb0 / 2);
+        int qt = it.next();
+        if (qt >= u.n_qt) continue;  // nothing visited: the warpgroups write zeros
+        if (ni >= 1) mbar_wait(kv_free, (ni - 1) & 1);
         if (leader) {
-          uint8_t* qdst = smem + C::kOffQ + s * 2 * C::kQBytes;
-          mbar_expect_tx(bar_qfull + s, 2 * C::kQBytes);
-          for (int c = 0; c < D / 64; ++c) {
-            tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64,
-                        u.trow0 + qt * kTileM, h, u.tb);
-            tma_load_4d(&tm_do, bar_qfull + s, qdst + C::kQBytes + c * (kTileM * 128), c * 64,
-                        u.trow0 + qt * kTileM, h, u.tb);
-          }
+          // both key blocks; rows past L (odd nb) are zero-filled by the TMA
+          mbar_expect_tx(bar_kv, 2 * C::kPairBytes);
+          for (int w = 0; w < 2; ++w)  // the K/V tensor maps have 64-row boxes
+            for (int c = 0; c < D / 64; ++c) {
+              const int off = c * (2 * kBlock * 128) + w * (kBlock * 128);
+              tma_load_4d(&tm_k, bar_kv, smem + C::kOffK + off, c * 64,
+                          u.trow0 + (wi.kb0 + w) * kBlock, wi.h, u.tb);
+              tma_load_4d(&tm_v, bar_kv, smem + C::kOffV + off, c * 64,
+                          u.trow0 + (wi.kb0 + w) * kBlock, wi.h, u.tb);
+            }
         }
         __syncwarp();
+        for (; qt < u.n_qt; qt = it.next(), ++jg) {
+          const int s = jg % ST;
+          if (jg >= ST) mbar_wait(bar_qempty + s, ((jg / ST) - 1) & 1);
+          SB_TR(args, 2, jg, 12);
+          if (leader) {
+            uint8_t* qdst = smem + C::kOffQ + s * 2 * C::kQBytes;
+            mbar_expect_tx(bar_qfull + s, 2 * C::kQBytes);
+            for (int c = 0; c < D / 64; ++c) {
+              tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64,
+                          u.trow0 + qt * kTileM, wi.h, u.tb);
+              tma_load_4d(&tm_do, bar_qfull + s, qdst + C::kQBytes + c * (kTileM * 128), c * 64,
+                          u.trow0 + qt * kTileM, wi.h, u.tb);
+            }
+          }
+          __syncwarp();
+        }
+        ++ni;
       }
-    } else if (warp == 9 && any) {
+    } else if (warp == 9) {
       // ---------------------------------------------------------- MMA issuer
       // whole warp: uniform control flow and descriptors; one elected lane issues.
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);  // Q K^T, dO V^T (N = 2 blocks)
-      constexpr uint32_t idesc_t = idesc_bf16(D, 128, 1, 1);    // dO^T A, Q^T dZ: MN-major
+      // dV = A^T dO, dK = dZ^T Q: M = 128 keys, N = D; A^T / dZ^T and dO / Q are read
+      // straight from their row-major tiles as MN-major operands
+      constexpr uint32_t idesc_t = idesc_bf16(128, D, 1, 1);
       const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
       const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), 16, 1024);
       const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
       const uint64_t dqmn = sdesc_sw128(smem_u32(smem + C::kOffQ), kTileM * 128, 1024);
       const uint64_t daz = sdesc_sw128(smem_u32(smem + C::kOffAZ), C::kPBytes, 1024);
       const bool leader = elect_one();
-      int n = 1;
-      for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
-      mbar_wait(bar_kv, 0);
       // Fixed issue order matching the warpgroups' event order:
-      // dV^T(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1) landed], dW(j+1)
-      // [dW(j) read], dK^T(j) [dZ(j) in smem].
-      auto issue_s = [&](int j) {
-        const uint32_t qo = (j % ST) * 2 * C::kQBytes;
-        mbar_wait(bar_qfull + j % ST, (j / ST) & 1);
-        SB_TR(args, 2, j, 13);
-        if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
-        SB_TR(args, 2, j, 8);
+      // dV(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1) landed], dW(j+1)
+      // [dW(j) read], dK(j) [dZ(j) in smem].
+      auto issue_s = [&](int jg) {
+        const uint32_t qo = (jg % ST) * 2 * C::kQBytes;
+        mbar_wait(bar_qfull + jg % ST, (jg / ST) & 1);
+        SB_TR(args, 2, jg, 13);
+        if (jg >= 1) mbar_wait(sempty, (jg - 1) & 1);
+        SB_TR(args, 2, jg, 8);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -654,10 +685,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       };
-      auto issue_w = [&](int j) {  // Q/dO stage already landed (issue_s(j) waited)
-        const uint32_t dof = (j % ST) * 2 * C::kQBytes + C::kQBytes;
-        if (j >= 1) mbar_wait(wempty, (j - 1) & 1);
-        SB_TR(args, 2, j, 10);
+      auto issue_w = [&](int jg, bool last) {  // Q/dO stage already landed (issue_s waited)
+        const uint32_t dof = (jg % ST) * 2 * C::kQBytes + C::kQBytes;
+        if (jg >= 1) mbar_wait(wempty, (jg - 1) & 1);
+        SB_TR(args, 2, jg, 10);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -667,42 +698,57 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             umma_ss(tW, desc_add(dq, dof + off), desc_add(dv, offk), idesc_s, k > 0);
           }
           umma_commit(wfull);
+          if (last) umma_commit(kv_free);  // the item's K/V pair may be replaced
         }
         __syncwarp();
       };
-      issue_s(0);
-      issue_w(0);
-      for (int j = 0; j < n; ++j) {
-        const int s = j % ST;
-        const uint32_t qo = s * 2 * C::kQBytes, dof = qo + C::kQBytes;
-        mbar_wait(afull, j & 1);
-        SB_TR(args, 2, j, 9);
-        tc_fence_after();
-        if (leader) {
+      int jg = 0, ni = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const KVItem wi = kv_item(g, idx);
+        if (!wi.valid) continue;
+        const Unit& u = wi.u;
+        LiveQt it{args.first_kb + u.fkb_off, u.nb, u.n_qt, wi.kb0, 0, wi.kb0, 0, 0u, 0u};
+        it.fill(wi.kb0 / 2);
+        int n = 0;
+        for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
+        if (n == 0) continue;
+        mbar_wait(bar_kv, ni & 1);
+        issue_s(jg);
+        issue_w(jg, n == 1);
+        for (int j = 0; j < n; ++j, ++jg) {
+          const int s = jg % ST;
+          const uint32_t qo = s * 2 * C::kQBytes, dof = qo + C::kQBytes;
+          mbar_wait(afull, jg & 1);
+          // the previous item's dV/dK must be out of TMEM before overwriting
+          if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);
+          SB_TR(args, 2, jg, 9);
+          tc_fence_after();
+          if (leader) {
 #pragma unroll
-          for (int k = 0; k < kTileM / 16; ++k)  // dV^T += dO^T A  (K = query rows)
-            umma_ss(tV, desc_add(dqmn, dof + k * 2048), desc_add(daz, k * 2048), idesc_t,
-                    (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(aused);
-        }
-        __syncwarp();
-        if (j + 1 < n) issue_s(j + 1);
-        if (j + 1 < n) issue_w(j + 1);
-        mbar_wait(zfull, j & 1);
-        SB_TR(args, 2, j, 11);
-        tc_fence_after();
-        if (leader) {
+            for (int k = 0; k < kTileM / 16; ++k)  // dV += A^T dO  (K = query rows)
+              umma_ss(tV, desc_add(daz, k * 2048), desc_add(dqmn, dof + k * 2048), idesc_t,
+                      (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(aused);
+          }
+          __syncwarp();
+          if (j + 1 < n) issue_s(jg + 1);
+          if (j + 1 < n) issue_w(jg + 1, j + 2 == n);
+          mbar_wait(zfull, jg & 1);
+          SB_TR(args, 2, jg, 11);
+          tc_fence_after();
+          if (leader) {
 #pragma unroll
-          for (int k = 0; k < kTileM / 16; ++k)  // dK^T += Q^T dZ
-            umma_ss(tK, desc_add(dqmn, qo + k * 2048), desc_add(daz, k * 2048), idesc_t,
-                    (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(zused);
-          umma_commit(bar_qempty + s);
+            for (int k = 0; k < kTileM / 16; ++k)  // dK += dZ^T Q
+              umma_ss(tK, desc_add(daz, k * 2048), desc_add(dqmn, qo + k * 2048), idesc_t,
+                      (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(zused);
+            umma_commit(bar_qempty + s);
+            if (j + 1 == n) umma_commit(done);
+          }
+          __syncwarp();
         }
-        __syncwarp();
+        ++ni;
       }
-      if (leader) umma_commit(done);
-      __syncwarp();
     }
   } else {
     reg_alloc<kRegsHighKV>();
@@ -710,113 +756,129 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int w = warp >> 2;
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
-    const int kb = kb0 + w;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t tSw = tS + lane_base + w * 64, tWw = tW + lane_base + w * 64;
-    const float* Mbase = args.M + u.m_off + (r & 63);
-    const float* Nbase = args.N + u.m_off + (r & 63);
     const uint32_t az_row = smem_u32(smem + C::kOffAZ + w * C::kPBytes) + r * 128;
-    // Per-tile operands: M (needed first) and the liveness of the next tile are
-    // obtained half a tile ahead; N and the row offset at the top of their own tile
-    // (consumed after the recompute).  Indices are clamped so every load is in
-    // bounds whether or not the tile is live.
-    auto tix = [&](int qt) -> int64_t {
-      const int qb = min(2 * qt + (r >> 6), u.nb - 1);
-      return tile_index(qb, min(kb, qb)) * kBlock;
-    };
-    auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < u.L; };
-    const bool tr = quarter == 0 && lane == 0;
-    if (tr) SB_TR(args, w, 0, 14);
-    int qt = qt_first;
-    bool live = is_live(qt);
-    float Ma = Mbase[tix(qt)];
-    for (int j = 0; qt < u.n_qt; ++j) {
-      const int my_qb = 2 * qt + (r >> 6);
-      const float Nb = Nbase[tix(qt)];
-      const float off =
-          args.row_offset
-              ? args.row_offset[u.rem_off + min(qt * kTileM + r, u.L - 1) * u.rem_stride]
-              : 0.0f;
-      const float E = live ? ex2(Ma) : 0.0f;  // dead rows/tiles: A = 0, dZ = 0
-      if (tr) SB_TR(args, w, j, 0);
-      mbar_wait(sfull, j & 1);
-      tc_fence_after();
-      float s[64], sg[64];
-      tmem_ld32(tSw, s);
-      tmem_ld32(tSw + 32, s + 32);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
-      if (tr) SB_TR(args, w, j, 1);
-      const bool diag = kb == my_qb;  // warp-uniform
-      if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
-      else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
-      if (tr) SB_TR(args, w, j, 2);
-      const int qt_next = it.next();  // warp-collective
-      const bool live_next = is_live(qt_next);
-      const float Ma_next = Mbase[tix(qt_next)];
-      uint32_t pk[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
-      if (j >= 1) mbar_wait(zused, (j - 1) & 1);  // dK^T of the previous tile read the buffer
-      if (tr) SB_TR(args, w, j, 8);
-      store_row_sw128(az_row, r, pk);
-      fence_proxy_async_smem();
-      mbar_arrive(afull);
-      if (tr) SB_TR(args, w, j, 3);
-      mbar_wait(wfull, j & 1);
-      tc_fence_after();
-      if (args.row_offset) load_dat<true>(s, tWw, off);  // warp-collective
-      else load_dat<false>(s, tWw, off);
-      tc_fence_before();
-      mbar_arrive(wempty);
-      if (tr) SB_TR(args, w, j, 4);
-      dz_row(s, sg, live ? Nb : 0.0f, pk);
-      if (tr) SB_TR(args, w, j, 5);
-      mbar_wait(aused, j & 1);  // dV^T of this tile read A
-      if (tr) SB_TR(args, w, j, 6);
-      store_row_sw128(az_row, r, pk);
-      fence_proxy_async_smem();
-      mbar_arrive(zfull);
-      if (tr) SB_TR(args, w, j, 7);
-      qt = qt_next;
-      live = live_next;
-      Ma = Ma_next;
-    }
-
-    // epilogue: dV^T / dK^T in TMEM (lanes = head-dim index, columns = keys of the
-    // pair; this warpgroup writes key block kb = columns w*64 ..).
-    // M = 128: lane r <-> d = r.  M = 64: rows 16q+i live in lanes 32q+i, i < 16.
-    const int dlane = (D == 128) ? r : (lane < 16 ? (quarter * 16 + lane) : -1);
-    if (any) {
-      mbar_wait(done, 0);
-      if (tr) SB_TR(args, w, 0, 15);
-      tc_fence_after();
-    }
     const float scale = g.scale_log2 * kLn2;
-    const int64_t base = u.out_off;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      float vv[32], kk[32];
-      if (any) {
-        tmem_ld32(tV + lane_base + w * 64 + half * 32, vv);
-        tmem_ld32(tK + lane_base + w * 64 + half * 32, kk);
+    const bool tr = quarter == 0 && lane == 0;
+    int jg = 0, ni = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const KVItem wi = kv_item(g, idx);
+      if (!wi.valid) continue;
+      const Unit& u = wi.u;
+      const int kb = wi.kb0 + w;
+      // half = which 64-row half of the query tile this warp's rows are in
+      LiveQt it{args.first_kb + u.fkb_off, u.nb, u.n_qt, wi.kb0, quarter >> 1, kb, 0, 0u, 0u};
+      it.fill(wi.kb0 / 2);  // query tile kb0/2 holds the diagonal of key block kb0
+      int qt = it.next();
+      const bool any = qt < u.n_qt;
+      const float* Mbase = args.M + u.m_off + (r & 63);
+      const float* Nbase = args.N + u.m_off + (r & 63);
+      // Per-tile operands: M (needed first) and the liveness of the next tile are
+      // obtained half a tile ahead; N and the row offset at the top of their own
+      // tile (consumed after the recompute).  Indices are clamped so every load is
+      // in bounds whether or not the tile is live.
+      auto tix = [&](int qt) -> int64_t {
+        const int qb = min(2 * qt + (r >> 6), u.nb - 1);
+        return tile_index(qb, min(kb, qb)) * kBlock;
+      };
+      auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < u.L; };
+      if (tr && ni == 0) SB_TR(args, w, 0, 14);
+      if (tr && jg >= 1) SB_TR(args, w, jg - 1, 11);
+      bool live = is_live(qt);
+      float Ma = Mbase[tix(qt)];
+      for (; qt < u.n_qt; ++jg) {
+        const int my_qb = 2 * qt + (r >> 6);
+        const float Nb = Nbase[tix(qt)];
+        const float off =
+            args.row_offset
+                ? args.row_offset[u.rem_off + min(qt * kTileM + r, u.L - 1) * u.rem_stride]
+                : 0.0f;
+        const float E = live ? ex2(Ma) : 0.0f;  // dead rows/tiles: A = 0, dZ = 0
+        if (tr) SB_TR(args, w, jg, 0);
+        mbar_wait(sfull, jg & 1);
+        tc_fence_after();
+        float s[64], sg[64];
+        tmem_ld32(tSw, s);
+        tmem_ld32(tSw + 32, s + 32);
         tmem_wait_ld();
-      } else {
+        tc_fence_before();
+        mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
+        if (tr) SB_TR(args, w, jg, 1);
+        const bool diag = kb == my_qb;  // warp-uniform
+        if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
+        else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
+        if (tr) SB_TR(args, w, jg, 2);
+        const int qt_next = it.next();  // warp-collective
+        const bool live_next = is_live(qt_next);
+        const float Ma_next = Mbase[tix(qt_next)];
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) vv[c] = kk[c] = 0.0f;
+        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
+        if (jg >= 1) mbar_wait(zused, (jg - 1) & 1);  // dK of the previous tile read the buffer
+        if (tr) SB_TR(args, w, jg, 8);
+        store_row_sw128(az_row, r, pk);
+        fence_proxy_async_smem();
+        mbar_arrive(afull);
+        if (tr) SB_TR(args, w, jg, 3);
+        mbar_wait(wfull, jg & 1);
+        tc_fence_after();
+        if (args.row_offset) load_dat<true>(s, tWw, off);  // warp-collective
+        else load_dat<false>(s, tWw, off);
+        tc_fence_before();
+        mbar_arrive(wempty);
+        if (tr) SB_TR(args, w, jg, 4);
+        dz_row(s, sg, live ? Nb : 0.0f, pk);
+        if (tr) SB_TR(args, w, jg, 5);
+        mbar_wait(aused, jg & 1);  // dV of this tile read A
+        if (tr) SB_TR(args, w, jg, 6);
+        store_row_sw128(az_row, r, pk);
+        fence_proxy_async_smem();
+        mbar_arrive(zfull);
+        if (tr) SB_TR(args, w, jg, 7);
+        qt = qt_next;
+        live = live_next;
+        Ma = Ma_next;
       }
-      if (dlane >= 0 && kb < u.nb) {
+
+      // epilogue: dV / dK in TMEM (lane = key of the pair, columns = head dim).
+      // Warp (w, quarter) owns keys 32*quarter .. +31 of the pair (lane = key) and
+      // head-dim columns w*D/2 .. +D/2; rows leave through this warp's 4 KB slice
+      // of the A/dZ buffers (free: the last dK MMA completed, `done`) as
+      // coalesced row segments.
+      if (any) {
+        mbar_wait(done, ni & 1);
+        tc_fence_after();
+      }
+      if (tr && jg >= 1) SB_TR(args, w, jg - 1, 9);
+      {
+        constexpr int HD = D / 2;
+        const int key0 = wi.kb0 * kBlock + quarter * 32;
+        const int nvalid = max(0, min(32, u.L - key0));
+        const uint32_t stage = smem_u32(smem + C::kOffAZ) + (warp & 7) * (32 * HD * 2);
+#pragma unroll 1
+        for (int t = 0; t < 2; ++t) {
+          float a[HD];
+          if (any) {
+            const uint32_t tacc = (t ? tK : tV) + lane_base + w * HD;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int key = kb * kBlock + half * 32 + c;
-          if (key < u.L) {
-            const int64_t o = base + (int64_t)key * g.sl + dlane;
-            args.dv[o] = __float2bfloat16_rn(vv[c]);
-            args.dk[o] = __float2bfloat16_rn(kk[c] * scale);
+            for (int c = 0; c < HD; c += 32) tmem_ld32(tacc + c, a + c);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int c = 0; c < HD; ++c) a[c] = 0.0f;
           }
+          if (tr && jg >= 1) SB_TR(args, w, jg - 1, 12 + t);
+          if (t == 1 && any) {
+            tc_fence_before();
+            mbar_arrive(acc_free);  // the next item's dV/dK may start
+          }
+          __nv_bfloat16* dst = (t ? args.dk : args.dv) + u.out_off + (int64_t)key0 * g.sl + w * HD;
+          warp_store_rows<HD / 8>(a, t ? scale : 1.0f, stage, dst, g.sl, nvalid);
         }
       }
+      if (tr && jg >= 1) SB_TR(args, w, jg - 1, 10);
+      if (any) ++ni;
     }
   }
   tc_fence_before();
@@ -844,8 +906,13 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
-    kern<<<(unsigned)((a.g.nb + 1) / 2) * BH, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tv,
-                                                                               a);
+    // persistent: one CTA per SM (fewer if there are fewer work items)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned items = (unsigned)((a.g.nb + 1) / 2) * BH;
+    kern<<<items < (unsigned)sms ? items : (unsigned)sms, kBwdThreads, C::kSmem, stream>>>(
+        tq, tdo, tk, tv, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   }
   return 0;

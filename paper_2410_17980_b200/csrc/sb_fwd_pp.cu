@@ -284,21 +284,19 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       // epilogue
       mbar_wait(bar_ofull + w, 0);
       tc_fence_after();
-      __nv_bfloat16* orow = args.o + u.out_off + (int64_t)row * g.sl;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        float ov[32];
-        tmem_ld32(tO + c * 32, ov);
+      // O rows leave in 64-column halves through this warp's 4 KB slice of the
+      // (now idle: ofull) P buffers as coalesced row segments
+      const int row0 = qt * kTileM + quarter * 32;
+      const int nvalid = max(0, min(32, u.L - row0));
+      const uint32_t stage = smem_u32(smem + C::kOffP + w * 2 * C::kPBytes) + quarter * 4096;
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        float ov[64];
+        tmem_ld32(tO + c * 64, ov);
+        tmem_ld32(tO + c * 64 + 32, ov + 32);
         tmem_wait_ld();
-        if (row_valid) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            dst[q4] = make_uint4(pack_bf16(ov[8 * q4], ov[8 * q4 + 1]),
-                                 pack_bf16(ov[8 * q4 + 2], ov[8 * q4 + 3]),
-                                 pack_bf16(ov[8 * q4 + 4], ov[8 * q4 + 5]),
-                                 pack_bf16(ov[8 * q4 + 6], ov[8 * q4 + 7]));
-        }
+        warp_store_rows<8>(ov, 1.0f, stage, args.o + u.out_off + (int64_t)row0 * g.sl + c * 64,
+                           g.sl, nvalid);
       }
       if (row_valid) args.log_rem[u.rem_off + row * u.rem_stride] = a2 * kLn2;
       if (my_qb < u.nb && (r & 63) == 0) {

@@ -230,4 +230,43 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                : "memory");
 }
 
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// Coalesced store of a warp's 32 rows (lane j holds row j: NCH*8 floats, times
+// `mul`, written as bf16).  A thread-per-row store scatters each 16-byte store
+// instruction over 32 rows (32 L1 transactions); here the rows are staged in
+// `stage` (32 * NCH * 16 bytes of shared memory owned by this warp, 128B-style
+// XOR swizzle: conflict-free), then every store instruction writes 32/NCH whole
+// row segments.  Rows j >= nvalid are not written.  dst0 = row 0's first column,
+// ld = row pitch in elements.
+template <int NCH>
+__device__ __forceinline__ void warp_store_rows(const float* v, float mul, uint32_t stage,
+                                                __nv_bfloat16* dst0, int64_t ld, int nvalid) {
+  const int lane = threadIdx.x & 31;
+  constexpr int RB = NCH * 16;  // bytes per row segment
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+    st_shared_v4(stage + lane * RB + ((c ^ (lane & (NCH - 1))) << 4),
+                 pack_bf16(v[8 * c] * mul, v[8 * c + 1] * mul),
+                 pack_bf16(v[8 * c + 2] * mul, v[8 * c + 3] * mul),
+                 pack_bf16(v[8 * c + 4] * mul, v[8 * c + 5] * mul),
+                 pack_bf16(v[8 * c + 6] * mul, v[8 * c + 7] * mul));
+  __syncwarp();
+  constexpr int RPS = 32 / NCH;  // rows per store instruction
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const int row = k * RPS + lane / NCH, c = lane % NCH;
+    const uint4 x = ld_shared_v4(stage + row * RB + ((c ^ (row & (NCH - 1))) << 4));
+    if (row < nvalid) *reinterpret_cast<uint4*>(dst0 + (int64_t)row * ld + c * 8) = x;
+  }
+  __syncwarp();
+}
+
 }  // namespace sb

@@ -30,14 +30,16 @@ __global__ void __launch_bounds__(544, 1) ub(int mode, int mma_kind, int nld, un
     if (lane == 0 && mode >= 1) {
       const uint32_t a = smem_u32(smem), b = smem_u32(smem + 64 * 1024);
       // kinds 0-3: one accumulator; 4: N=64 over 4 accumulators; 5: N=128 over 2; 6: N=256 over 2
-      const int N = (mma_kind == 2 || mma_kind == 5) ? 128 : (mma_kind == 3 || mma_kind == 6) ? 256 : 64;
-      const bool mn = mma_kind == 1;
+      const int N = (mma_kind == 2 || mma_kind == 5 || mma_kind == 7) ? 128
+                    : (mma_kind == 3 || mma_kind == 6) ? 256 : 64;
+      const bool mn = mma_kind == 1 || mma_kind == 7;
       const int nacc = mma_kind == 4 ? 4 : (mma_kind >= 5 ? 2 : 1);
       const uint32_t idesc = idesc_bf16(128, N, mn, mn);
       uint64_t ad[8], bd[8];
       for (int k = 0; k < 8; ++k) {
         ad[k] = mn ? sdesc_sw128(a + k * 2048, 16384, 1024) : sdesc_sw128(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-        bd[k] = mn ? sdesc_sw128(b + k * 2048, 16, 1024) : sdesc_sw128(b + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
+        bd[k] = mn ? sdesc_sw128(b + k * 2048, N > 64 ? 16384 : 16, 1024)
+                   : sdesc_sw128(b + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024);
       }
       const uint32_t cstep = mma_kind == 6 ? 256 : N;
       for (int it = 0; it < ITER; ++it) {
@@ -79,8 +81,8 @@ int main() {
   cudaMalloc(&d, 148 * 2 * 8);
   cudaFuncSetAttribute(ub, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
   const char* kn[] = {"128x64 K-major", "128x64 MN-major", "128x128 K-major", "128x256 K-major",
-                      "128x64 4 acc", "128x128 2 acc", "128x256 2 acc"};
-  const int Ns[] = {64, 64, 128, 256, 64, 128, 256};
+                      "128x64 4 acc", "128x128 2 acc", "128x256 2 acc", "128x128 MN/MN"};
+  const int Ns[] = {64, 64, 128, 256, 64, 128, 256, 128};
   std::vector<unsigned long long> h(296);
   auto run = [&](int mode, int kind, int nld) {
     cudaMemset(d, 0, 296 * 8);
@@ -107,7 +109,7 @@ int main() {
     printf("\n");
   };
   for (int nld : {4, 8, 16}) run(0, 0, nld);
-  for (int k = 0; k < 7; ++k) run(1, k, 0);
+  for (int k = 0; k < 8; ++k) run(1, k, 0);
   for (int nld : {4, 8}) run(2, 0, nld);
   run(2, 1, 8);
   for (int nld : {4, 8, 16}) run(3, 2, nld);
