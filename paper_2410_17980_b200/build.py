@@ -36,14 +36,21 @@ def _stale(lib: str = LIB) -> bool:
 LIB_TRACE = os.path.join(HERE, "libsbattn_trace.so")
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False,
+          variant: str = "") -> str:
     """Compile libsbattn.so (or, with trace=True, the -DSB_TRACE tuning variant
-    libsbattn_trace.so that records per-event SM clocks, tools/trace_kernels.py)."""
+    libsbattn_trace.so that records per-event SM clocks, tools/trace_kernels.py;
+    variant="nomath" builds libsbattn_nomath.so, the pipeline without the stick
+    math, for tools/ablate.py)."""
     lib = LIB_TRACE if trace else LIB
-    if not force and not _stale(lib):
-        return lib
     tag = "_trace" if trace else ""
     extra = ["-DSB_TRACE"] if trace else []
+    if variant:
+        lib = os.path.join(HERE, f"libsbattn_{variant}.so")
+        tag = "_" + variant
+        extra = ["-D" + {"nomath": "SB_NOMATH"}[variant]]
+    if not force and not _stale(lib):
+        return lib
     jobs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)

@@ -51,6 +51,11 @@ static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "
 template <bool kDiag>
 __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float E,
                                               int lim) {
+#ifdef SB_NOMATH  // tuning ablation: pipeline without the stick math
+#pragma unroll
+  for (int c = 0; c < kBlock; ++c) { s[c] *= E; sg[c] = E; }
+  return;
+#endif
   constexpr int NG = kBlock / 16;
   float tot[NG];
 #pragma unroll
@@ -466,10 +471,12 @@ struct BwdKVCfg {
   static constexpr int kPBytes = kTileM * kBlock * 2;    // A / dZ of one warpgroup
   static constexpr int kOffK = 0;                        // chunk c: rows 0..127 = K0;K1
   static constexpr int kOffV = kOffK + kPairBytes;
-  static constexpr int kOffQ = kOffV + kPairBytes;               // stage s: Q, dO
-  static constexpr int kOffAZ = kOffQ + kStages * 2 * kQBytes;   // WG0 then WG1 (contiguous)
-  static constexpr int kOffBar = kOffAZ + 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 11;
+  static constexpr int kOffQ = kOffV + kPairBytes;         // Q ring (kStages)
+  static constexpr int kOffDO = kOffQ + kStages * kQBytes;  // dO: one buffer (free after dV)
+  static constexpr int kOffA = kOffDO + kQBytes;            // A: WG0 then WG1 (contiguous)
+  static constexpr int kOffZ = kOffA + 2 * kPBytes;         // dZ: WG0 then WG1
+  static constexpr int kOffBar = kOffZ + 2 * kPBytes;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 11;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
@@ -560,7 +567,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_kv = bars;
   uint64_t* bar_qfull = bars + 1;
   uint64_t* bar_qempty = bar_qfull + ST;
-  uint64_t* sfull = bar_qempty + ST;  // S = Q K^T landed in TMEM
+  uint64_t* bar_dofull = bar_qempty + ST;  // dO of the current tile landed
+  uint64_t* bar_doempty = bar_dofull + 1;  // dV (its last reader) completed
+  uint64_t* sfull = bar_doempty + 1;  // S = Q K^T landed in TMEM
   uint64_t* sempty = sfull + 1;       // S read by both warpgroups
   uint64_t* wfull = sfull + 2;        // dW = dO V^T landed
   uint64_t* wempty = sfull + 3;       // dW read
@@ -579,6 +588,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(bar_qfull + s, 1);
       mbar_init(bar_qempty + s, 1);
     }
+    mbar_init(bar_dofull, 1);
+    mbar_init(bar_doempty, 1);
     mbar_init(sfull, 1);
     mbar_init(sempty, 256);
     mbar_init(wfull, 1);
@@ -638,14 +649,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (jg >= ST) mbar_wait(bar_qempty + s, ((jg / ST) - 1) & 1);
           SB_TR(args, 2, jg, 12);
           if (leader) {
-            uint8_t* qdst = smem + C::kOffQ + s * 2 * C::kQBytes;
-            mbar_expect_tx(bar_qfull + s, 2 * C::kQBytes);
-            for (int c = 0; c < D / 64; ++c) {
+            uint8_t* qdst = smem + C::kOffQ + s * C::kQBytes;
+            mbar_expect_tx(bar_qfull + s, C::kQBytes);
+            for (int c = 0; c < D / 64; ++c)
               tma_load_4d(&tm_q, bar_qfull + s, qdst + c * (kTileM * 128), c * 64,
                           u.trow0 + qt * kTileM, wi.h, u.tb);
-              tma_load_4d(&tm_do, bar_qfull + s, qdst + C::kQBytes + c * (kTileM * 128), c * 64,
+          }
+          __syncwarp();
+          if (jg >= 1) mbar_wait(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
+          if (leader) {
+            mbar_expect_tx(bar_dofull, C::kQBytes);
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_4d(&tm_do, bar_dofull, smem + C::kOffDO + c * (kTileM * 128), c * 64,
                           u.trow0 + qt * kTileM, wi.h, u.tb);
-            }
           }
           __syncwarp();
         }
@@ -662,13 +678,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), 16, 1024);
       const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
       const uint64_t dqmn = sdesc_sw128(smem_u32(smem + C::kOffQ), kTileM * 128, 1024);
-      const uint64_t daz = sdesc_sw128(smem_u32(smem + C::kOffAZ), C::kPBytes, 1024);
+      const uint64_t ddo = sdesc_sw128(smem_u32(smem + C::kOffDO), 16, 1024);
+      const uint64_t ddomn = sdesc_sw128(smem_u32(smem + C::kOffDO), kTileM * 128, 1024);
+      const uint64_t da = sdesc_sw128(smem_u32(smem + C::kOffA), C::kPBytes, 1024);
+      const uint64_t dz = sdesc_sw128(smem_u32(smem + C::kOffZ), C::kPBytes, 1024);
       const bool leader = elect_one();
       // Fixed issue order matching the warpgroups' event order:
       // dV(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1) landed], dW(j+1)
       // [dW(j) read], dK(j) [dZ(j) in smem].
       auto issue_s = [&](int jg) {
-        const uint32_t qo = (jg % ST) * 2 * C::kQBytes;
+        const uint32_t qo = (jg % ST) * C::kQBytes;
         mbar_wait(bar_qfull + jg % ST, (jg / ST) & 1);
         SB_TR(args, 2, jg, 13);
         if (jg >= 1) mbar_wait(sempty, (jg - 1) & 1);
@@ -679,14 +698,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
             const uint32_t offk = (k >> 2) * (2 * kBlock * 128) + (k & 3) * 32;
-            umma_ss(tS, desc_add(dq, qo + off), desc_add(dk, offk), idesc_s, k > 0);
+            umma_ss_at(tS, dq, qo + off, dk, offk, idesc_s, k > 0);
           }
           umma_commit(sfull);
         }
         __syncwarp();
       };
-      auto issue_w = [&](int jg, bool last) {  // Q/dO stage already landed (issue_s waited)
-        const uint32_t dof = (jg % ST) * 2 * C::kQBytes + C::kQBytes;
+      auto issue_w = [&](int jg, bool last) {
+        mbar_wait(bar_dofull, jg & 1);
         if (jg >= 1) mbar_wait(wempty, (jg - 1) & 1);
         SB_TR(args, 2, jg, 10);
         tc_fence_after();
@@ -695,7 +714,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
             const uint32_t offk = (k >> 2) * (2 * kBlock * 128) + (k & 3) * 32;
-            umma_ss(tW, desc_add(dq, dof + off), desc_add(dv, offk), idesc_s, k > 0);
+            umma_ss_at(tW, ddo, off, dv, offk, idesc_s, k > 0);
           }
           umma_commit(wfull);
           if (last) umma_commit(kv_free);  // the item's K/V pair may be replaced
@@ -715,9 +734,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(bar_kv, ni & 1);
         issue_s(jg);
         issue_w(jg, n == 1);
+        // Fixed issue order: dV(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1)
+        // landed], dK(j) [dZ(j) in smem], dW(j+1) [dW(j) read, dO(j+1) landed:
+        // dO is single-buffered, reloaded once dV(j) has read it].
         for (int j = 0; j < n; ++j, ++jg) {
           const int s = jg % ST;
-          const uint32_t qo = s * 2 * C::kQBytes, dof = qo + C::kQBytes;
+          const uint32_t qo = s * C::kQBytes;
           mbar_wait(afull, jg & 1);
           // the previous item's dV/dK must be out of TMEM before overwriting
           if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);
@@ -726,26 +748,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (leader) {
 #pragma unroll
             for (int k = 0; k < kTileM / 16; ++k)  // dV += A^T dO  (K = query rows)
-              umma_ss(tV, desc_add(daz, k * 2048), desc_add(dqmn, dof + k * 2048), idesc_t,
+              umma_ss_at(tV, da, k * 2048, ddomn, k * 2048, idesc_t,
                       (j > 0 || k > 0) ? 1u : 0u);
             umma_commit(aused);
+            umma_commit(bar_doempty);
           }
           __syncwarp();
           if (j + 1 < n) issue_s(jg + 1);
-          if (j + 1 < n) issue_w(jg + 1, j + 2 == n);
           mbar_wait(zfull, jg & 1);
           SB_TR(args, 2, jg, 11);
           tc_fence_after();
           if (leader) {
 #pragma unroll
             for (int k = 0; k < kTileM / 16; ++k)  // dK += dZ^T Q
-              umma_ss(tK, desc_add(daz, k * 2048), desc_add(dqmn, qo + k * 2048), idesc_t,
+              umma_ss_at(tK, dz, k * 2048, dqmn, qo + k * 2048, idesc_t,
                       (j > 0 || k > 0) ? 1u : 0u);
             umma_commit(zused);
             umma_commit(bar_qempty + s);
             if (j + 1 == n) umma_commit(done);
           }
           __syncwarp();
+          if (j + 1 < n) issue_w(jg + 1, j + 2 == n);
         }
         ++ni;
       }
@@ -758,7 +781,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t tSw = tS + lane_base + w * 64, tWw = tW + lane_base + w * 64;
-    const uint32_t az_row = smem_u32(smem + C::kOffAZ + w * C::kPBytes) + r * 128;
+    const uint32_t a_row = smem_u32(smem + C::kOffA + w * C::kPBytes) + r * 128;
+    const uint32_t z_row = smem_u32(smem + C::kOffZ + w * C::kPBytes) + r * 128;
     const float scale = g.scale_log2 * kLn2;
     const bool tr = quarter == 0 && lane == 0;
     int jg = 0, ni = 0;
@@ -815,9 +839,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
-        if (jg >= 1) mbar_wait(zused, (jg - 1) & 1);  // dK of the previous tile read the buffer
+        if (jg >= 1) mbar_wait(aused, (jg - 1) & 1);  // dV of the previous tile read A
         if (tr) SB_TR(args, w, jg, 8);
-        store_row_sw128(az_row, r, pk);
+        store_row_sw128(a_row, r, pk);
         fence_proxy_async_smem();
         mbar_arrive(afull);
         if (tr) SB_TR(args, w, jg, 3);
@@ -830,9 +854,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (tr) SB_TR(args, w, jg, 4);
         dz_row(s, sg, live ? Nb : 0.0f, pk);
         if (tr) SB_TR(args, w, jg, 5);
-        mbar_wait(aused, jg & 1);  // dV of this tile read A
+        if (jg >= 1) mbar_wait(zused, (jg - 1) & 1);  // dK of the previous tile read dZ
         if (tr) SB_TR(args, w, jg, 6);
-        store_row_sw128(az_row, r, pk);
+        store_row_sw128(z_row, r, pk);
         fence_proxy_async_smem();
         mbar_arrive(zfull);
         if (tr) SB_TR(args, w, jg, 7);
@@ -844,7 +868,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // epilogue: dV / dK in TMEM (lane = key of the pair, columns = head dim).
       // Warp (w, quarter) owns keys 32*quarter .. +31 of the pair (lane = key) and
       // head-dim columns w*D/2 .. +D/2; rows leave through this warp's 4 KB slice
-      // of the A/dZ buffers (free: the last dK MMA completed, `done`) as
+      // of the A buffers (free: every MMA of the item completed, `done`) as
       // coalesced row segments.
       if (any) {
         mbar_wait(done, ni & 1);
@@ -855,7 +879,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         constexpr int HD = D / 2;
         const int key0 = wi.kb0 * kBlock + quarter * 32;
         const int nvalid = max(0, min(32, u.L - key0));
-        const uint32_t stage = smem_u32(smem + C::kOffAZ) + (warp & 7) * (32 * HD * 2);
+        const uint32_t stage = smem_u32(smem + C::kOffA) + (warp & 7) * (32 * HD * 2);
 #pragma unroll 1
         for (int t = 0; t < 2; ++t) {
           float a[HD];

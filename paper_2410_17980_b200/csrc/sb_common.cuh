@@ -171,6 +171,12 @@ constexpr float kBatchedMax = 1.8446744073709552e19f;  // 2^64
 template <bool kDiag>
 __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_log2, int lim,
                                             float& Q, float& Dhi, float& Dlo) {
+#ifdef SB_NOMATH  // tuning ablation: pipeline without the stick math
+#pragma unroll
+  for (int c = 0; c < kBlock; c += 2) pk[c >> 1] = pack_bf16(s[c] * Q, s[c + 1] * Q);
+  Dhi = Dlo = 1.0f;
+  return true;
+#endif
   // pass 1: t into s[] and the group products, four independent chains
   constexpr int NG = kBlock / 16;
   float P[NG];

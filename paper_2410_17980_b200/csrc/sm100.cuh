@@ -184,6 +184,22 @@ __device__ __forceinline__ bool elect_one() {
 // field is the low 14 bits (address >> 4) and smem addresses stay below 256 KB.
 __device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 
+// umma_ss on (descriptor base + byte offsets): the 64-bit adds happen inside the
+// asm, so the compiler keeps only the bases (and 32-bit offsets) live instead of
+// hoisting every per-k descriptor into a 64-bit register pair.
+__device__ __forceinline__ void umma_ss_at(uint32_t d_tmem, uint64_t abase, uint32_t aoff,
+                                           uint64_t bbase, uint32_t boff, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a, b, oa, ob;\n\t"
+      "cvt.u64.u32 oa, %2;\n\tcvt.u64.u32 ob, %4;\n\t"
+      "add.s64 a, %1, oa;\n\tadd.s64 b, %3, ob;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, p;\n\t}" ::"r"(d_tmem),
+      "l"(abase), "r"(aoff >> 4), "l"(bbase), "r"(boff >> 4), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
