@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False,
     if variant:
         lib = os.path.join(HERE, f"libsbattn_{variant}.so")
         tag = "_" + variant
-        extra = ["-D" + {"nomath": "SB_NOMATH"}[variant]]
+        extra = {"nomath": ["-DSB_NOMATH"], "trace_nomath": ["-DSB_NOMATH", "-DSB_TRACE"]}[variant]
     if not force and not _stale(lib):
         return lib
     jobs = []

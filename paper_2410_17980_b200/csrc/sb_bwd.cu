@@ -157,17 +157,19 @@ __device__ __forceinline__ void store_row_sw128(uint32_t row_addr, int r, const 
 // Phase 1: dQ and N.  CTA = (b, h, query tiles 2p and 2p+1).
 template <int D>
 struct BwdQCfg {
-  static constexpr int kStages = 2;
+  // K ring of 3 stages (S(j) and dQ(j) read K(j): released at the end of tile j);
+  // V single-buffered (only dW(j) reads V(j): released early in tile j).
+  static constexpr int kStages = 3;
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kKVBytes = kBlock * D * 2;
   static constexpr int kZBytes = kTileM * kBlock * 2;
   static constexpr int kOffQ = 0;                       // Q[2]
   static constexpr int kOffDO = kOffQ + 2 * kQBytes;    // dO[2]
-  static constexpr int kOffK = kOffDO + 2 * kQBytes;
+  static constexpr int kOffK = kOffDO + 2 * kQBytes;    // K ring
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
-  static constexpr int kOffZ = kOffV + kStages * kKVBytes;  // Z[2] (one per WG)
+  static constexpr int kOffZ = kOffV + kKVBytes;        // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 7 + 1;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 * 7;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -205,18 +207,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* bar_qdo = bars;
   uint64_t* bar_kfull = bars + 1;
-  uint64_t* bar_vfull = bar_kfull + ST;
-  uint64_t* bar_kvempty = bar_vfull + ST;
-  uint64_t* wgbars = bar_kvempty + ST;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done
+  uint64_t* bar_kempty = bar_kfull + ST;
+  uint64_t* bar_vfull = bar_kempty + ST;
+  uint64_t* bar_vempty = bar_vfull + 1;
+  uint64_t* wgbars = bar_vempty + 1;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qdo, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_kfull + s, 1);
-      mbar_init(bar_vfull + s, 1);
-      mbar_init(bar_kvempty + s, has1 ? 2 : 1);
+      mbar_init(bar_kempty + s, has1 ? 2 : 1);  // dQ of each warpgroup read K
     }
+    mbar_init(bar_vfull, 1);
+    mbar_init(bar_vempty, has1 ? 2 : 1);  // dW of each warpgroup read V
     for (int w = 0; w < 2; ++w) {
       mbar_init(wgbars + w * 7 + 0, 1);    // sfull: S = Q K^T landed in TMEM
       mbar_init(wgbars + w * 7 + 1, 128);  // sempty: S read into registers
@@ -226,7 +230,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(wgbars + w * 7 + 5, 1);    // zempty: dQ MMA read dZ
       mbar_init(wgbars + w * 7 + 6, 1);    // done
     }
-    mbar_init(wgbars + 14, 128);  // stagger: WG0 finished its first recompute
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -255,17 +258,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       for (int j = 0; j < n_s; ++j) {
         const int s = j % ST;
-        if (j >= ST) mbar_wait(bar_kvempty + s, ((j / ST) - 1) & 1);
+        if (j >= ST) mbar_wait(bar_kempty + s, ((j / ST) - 1) & 1);
         SB_TR(args, 2, j, 12);
         const int kb = kb_lo + j;
         mbar_expect_tx(bar_kfull + s, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d(&tm_k, bar_kfull + s, smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128),
                       c * 64, u.trow0 + kb * kBlock, h, u.tb);
-        mbar_expect_tx(bar_vfull + s, C::kKVBytes);
+        if (j >= 1) mbar_wait(bar_vempty, (j - 1) & 1);
+        mbar_expect_tx(bar_vfull, C::kKVBytes);
         for (int c = 0; c < D / 64; ++c)
-          tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
+          tma_load_4d(&tm_v, bar_vfull, smem + C::kOffV + c * (kBlock * 128), c * 64,
+                      u.trow0 + kb * kBlock, h, u.tb);
       }
     }
   } else if (warp == 9 || warp == 10) {
@@ -286,9 +290,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
       const bool leader = elect_one();
       mbar_wait(bar_qdo, 0);
-      // Static issue order matching the stick warpgroup's event order:
-      // S(j+1) once S(j) was read, dW(j+1) once dW(j) was read, dQ(j) once dZ(j)
-      // is in smem.  S of tile j+1 runs while the warpgroup still works on tile j.
+      // Static issue order: S(j+1) once S(j) was read (it runs while the
+      // warpgroup still works on tile j), dQ(j) once dZ(j) is in smem, dW(j+1)
+      // once dW(j) was read and V(j+1) landed (V is single-buffered).
       auto issue_s = [&](int j) {
         const int s = j % ST;
         mbar_wait(bar_kfull + s, (j / ST) & 1);
@@ -301,15 +305,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
             const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-            umma_ss(tS, desc_add(dq, off), desc_add(dk, s * C::kKVBytes + offk), idesc_s, k > 0);
+            umma_ss_at(tS, dq, off, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
           }
           umma_commit(sfull);
         }
         __syncwarp();
       };
       auto issue_w = [&](int j) {
-        const int s = j % ST;
-        mbar_wait(bar_vfull + s, (j / ST) & 1);
+        mbar_wait(bar_vfull, j & 1);
         if (j >= 1) mbar_wait(wempty, (j - 1) & 1);
         SB_TR(args, 2 + w, j, 10);
         tc_fence_after();
@@ -318,9 +321,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
             const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-            umma_ss(tW, desc_add(ddo, off), desc_add(dv, s * C::kKVBytes + offk), idesc_s, k > 0);
+            umma_ss_at(tW, ddo, off, dv, offk, idesc_s, k > 0);
           }
           umma_commit(wfull);
+          umma_commit(bar_vempty);
         }
         __syncwarp();
       };
@@ -328,7 +332,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       issue_w(0);
       for (int j = 0; j < n_w; ++j) {
         if (j + 1 < n_w) issue_s(j + 1);
-        if (j + 1 < n_w) issue_w(j + 1);
         const int s = j % ST;
         mbar_wait(zfull, j & 1);
         SB_TR(args, 2 + w, j, 11);
@@ -336,18 +339,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (leader) {
 #pragma unroll
           for (int k = 0; k < kBlock / 16; ++k)
-            umma_ss(tQ, desc_add(dz, k * 32), desc_add(dkmn, s * C::kKVBytes + k * 2048), idesc_q,
+            umma_ss_at(tQ, dz, k * 32, dkmn, s * C::kKVBytes + k * 2048, idesc_q,
                     (j > 0 || k > 0) ? 1u : 0u);
           umma_commit(zempty);
-          umma_commit(bar_kvempty + s);
+          umma_commit(bar_kempty + s);
         }
         __syncwarp();
+        if (j + 1 < n_w) issue_w(j + 1);
       }
       if (leader) umma_commit(done);
       __syncwarp();
       for (int j = n_w; j < n_s; ++j) {  // stream tiles right of this WG's diagonal
-        mbar_wait(bar_vfull + j % ST, (j / ST) & 1);
-        if (leader) mbar_arrive(bar_kvempty + j % ST);
+        // release each buffer in its own phase: wait until tile j occupies it
+        mbar_wait(bar_kfull + j % ST, (j / ST) & 1);
+        if (leader) mbar_arrive(bar_kempty + j % ST);
+        mbar_wait(bar_vfull, j & 1);
+        if (leader) mbar_arrive(bar_vempty);
+        __syncwarp();
       }
     }
   }
@@ -388,9 +396,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const float E = live ? ex2(Ma) : 0.0f;
         if (j + 1 < n_w) Ma = Mrow[tile_of(kb + 1)];
         if (tr) SB_TR(args, w, j, 0);
-        // WG1 starts half a tile behind WG0 so the two warpgroups' latency-bound
-        // phases interleave on each SMSP instead of running in lockstep
-        if (j == 0 && w == 1) mbar_wait(wgbars + 14, 0);
         mbar_wait(sfull, j & 1);
         tc_fence_after();
         float s[64], sg[64];
@@ -405,7 +410,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
         else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
         if (tr) SB_TR(args, w, j, 2);
-        if (j == 0 && w == 0) mbar_arrive(wgbars + 14);
         mbar_wait(wfull, j & 1);
         tc_fence_after();
         if (args.row_offset) load_dat<true>(s, tW, off);

@@ -31,8 +31,9 @@ def main():
     ap.add_argument("--H", type=int, default=16)
     ap.add_argument("--L", type=int, default=4096)
     ap.add_argument("--D", type=int, default=128)
+    ap.add_argument("--lib", default="", help="prebuilt trace library (e.g. libsbattn_trace_nomath.so)")
     a = ap.parse_args()
-    path = build.build(trace=True)
+    path = a.lib or build.build(trace=True)
     lib = _lib.load(path)
     _lib._lib = lib  # route the ops through the trace build
     lib.sb_debug_set_trace.argtypes = [ctypes.c_void_p]
