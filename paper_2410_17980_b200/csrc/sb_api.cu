@@ -97,7 +97,7 @@ extern "C" {
 size_t sb_snapshot_elems(const sb_params_t* p) {
   if (!p || p->seqlen < 1) return 0;
   const size_t nb = (size_t)(p->seqlen + 63) / 64;
-  return (size_t)p->batch * p->heads * (nb * (nb + 1) / 2) * 64;
+  return sb::kSchedHeader + (size_t)p->batch * p->heads * (nb * (nb + 1) / 2) * 64;
 }
 
 int sb_varlen_elems(const sb_params_t* p, const int32_t* cu, size_t* snapshot,
@@ -111,7 +111,7 @@ int sb_varlen_elems(const sb_params_t* p, const int32_t* cu, size_t* snapshot,
     tiles += nb * (nb + 1) / 2;
     nbs += nb;
   }
-  *snapshot = (size_t)p->heads * tiles * 64;
+  *snapshot = sb::kSchedHeader + (size_t)p->heads * tiles * 64;
   *first_kb = (size_t)p->heads * nbs;
   return SB_OK;
 }
@@ -137,6 +137,7 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
   a.log_eps = std::log(eps);
   a.trace = g_trace;
+  a.sched = reinterpret_cast<unsigned*>(M);
   // skip on: exact log-space kernel (bit-exact skip decisions); skip off: the
   // ping-pong product-form kernel
   cudaStream_t st_ = reinterpret_cast<cudaStream_t>(stream);
@@ -178,6 +179,7 @@ int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void*
   a.M = M;
   a.N = N;
   a.trace = g_trace;
+  a.sched = reinterpret_cast<unsigned*>(N);
   int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, a, phases,
                             reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;

@@ -13,6 +13,7 @@ struct FwdArgs {
   unsigned long long* counters;  // [2]: visited tiles, total tiles (nullable)
   double log_eps;        // log(skip_eps)
   uint32_t* trace;       // SB_TRACE builds only (libsbattn_trace.so); null otherwise
+  unsigned* sched;       // work-queue counter (M header), zeroed before the launch
 };
 
 struct BwdArgs {
@@ -25,6 +26,7 @@ struct BwdArgs {
   const float* M;           // forward snapshots (log2 units)
   float* N;                 // phase-1 b snapshots, read by phase 2
   uint32_t* trace;          // SB_TRACE builds only (libsbattn_trace.so); null otherwise
+  unsigned* sched;          // work-queue counters [2] (N header), zeroed before the launch
 };
 
 // Event timeline for kernel tuning (tools/trace_kernels.py).  Compiled only with

@@ -480,7 +480,7 @@ struct BwdKVCfg {
   static constexpr int kOffA = kOffDO + kQBytes;            // A: WG0 then WG1 (contiguous)
   static constexpr int kOffZ = kOffA + 2 * kPBytes;         // dZ: WG0 then WG1
   static constexpr int kOffBar = kOffZ + 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 11;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 11 + 8;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
@@ -527,6 +527,9 @@ struct LiveQt {
   }
 };
 
+// Phase 2 work distribution: dynamic queue (SchedRing) or static striding.
+constexpr bool kDynamicKV = false;
+
 // Work item of phase 2: (unit, key pair p).  Every role derives the same item
 // list, so they agree on which items carry work without communicating.
 struct KVItem {
@@ -546,8 +549,8 @@ __device__ __forceinline__ KVItem kv_item(const Geom& g, int idx) {
   return it;
 }
 
-// Persistent: one CTA per SM walks the items idx = blockIdx.x, +gridDim.x, ...
-// (LPT order within groups of 8 units).  The Q/dO ring and every per-tile
+// Persistent: one CTA per SM takes items from a global work queue (LPT order
+// within groups of 8 units, handed out dynamically).  The Q/dO ring and every per-tile
 // barrier run on a CTA-wide tile counter across items, so the producer fetches
 // the next item's K/V and first Q/dO tiles while the warpgroups finish the
 // current item and write its dK/dV.  Per item: bar_kv (K/V landed), kv_free
@@ -585,6 +588,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* kv_free = sfull + 9;      // item's last S / dW read K/V
   uint64_t* acc_free = sfull + 10;    // dV/dK read out of TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+  const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), sfull + 11, sfull + 15};
 
   if (threadIdx.x == 0) {
     mbar_init(bar_kv, 1);
@@ -605,6 +609,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(done, 1);
     mbar_init(kv_free, 1);
     mbar_init(acc_free, 256);
+    sched_init(sq, 9);  // consumers: stick warps 0-7, issuer warp 9
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -626,7 +631,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_prefetch(&tm_v);
       }
       int jg = 0, ni = 0;  // tiles and work items so far
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      for (int kq = 0;; ++kq) {
+        const int idx = kDynamicKV ? sched_produce(sq, kq, args.sched + 1, n_items)
+                                   : (int)blockIdx.x + kq * (int)gridDim.x;
+        if (idx < 0 || idx >= n_items) break;
         const KVItem wi = kv_item(g, idx);
         if (!wi.valid) continue;
         const Unit& u = wi.u;
@@ -726,7 +734,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
       };
       int jg = 0, ni = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      for (int kq = 0;; ++kq) {
+        const int idx = kDynamicKV ? sched_consume(sq, kq) : (int)blockIdx.x + kq * (int)gridDim.x;
+        if (idx < 0 || idx >= n_items) break;
         const KVItem wi = kv_item(g, idx);
         if (!wi.valid) continue;
         const Unit& u = wi.u;
@@ -790,7 +800,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float scale = g.scale_log2 * kLn2;
     const bool tr = quarter == 0 && lane == 0;
     int jg = 0, ni = 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (int kq = 0;; ++kq) {
+      const int idx = kDynamicKV ? sched_consume(sq, kq) : (int)blockIdx.x + kq * (int)gridDim.x;
+      if (idx < 0 || idx >= n_items) break;
       const KVItem wi = kv_item(g, idx);
       if (!wi.valid) continue;
       const Unit& u = wi.u;
@@ -924,6 +936,7 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(a.sched, 0, sizeof(unsigned), stream)) != cudaSuccess) return (int)e;
     kern<<<(unsigned)((a.g.n_qt + 1) / 2) * BH, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tv,
                                                                                   a);
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
@@ -934,6 +947,8 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(a.sched + 1, 0, sizeof(unsigned), stream)) != cudaSuccess)
+      return (int)e;
     // persistent: one CTA per SM (fewer if there are fewer work items)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

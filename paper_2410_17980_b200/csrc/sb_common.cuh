@@ -9,6 +9,10 @@
 namespace sb {
 
 constexpr int kBlock = 64;     // reference d_block (blocked.py:41): skip / M / N granularity
+// M and N arrays start with a 64-float header holding the persistent kernels'
+// work-queue counters (M[0]: forward; N[0]: phase 1, N[1]: phase 2), zeroed by
+// the launcher before each kernel; the tile snapshots follow.
+constexpr int kSchedHeader = 64;
 constexpr int kTileM = 128;    // query rows per CTA tile = two 64-row skip groups
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -52,7 +56,7 @@ __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
     u.n_tiles = g.n_tiles;
     u.trow0 = 0;
     u.tb = b;
-    u.m_off = unit * g.n_tiles * kBlock;
+    u.m_off = kSchedHeader + unit * g.n_tiles * kBlock;
     u.fkb_off = unit * g.nb;
     u.rem_off = unit * g.L;
     u.rem_stride = 1;
@@ -71,7 +75,7 @@ __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
     u.n_tiles = (int64_t)u.nb * (u.nb + 1) / 2;
     u.trow0 = s0;
     u.tb = 0;
-    u.m_off = (tiles_before * g.H + (int64_t)h * u.n_tiles) * kBlock;
+    u.m_off = kSchedHeader + (tiles_before * g.H + (int64_t)h * u.n_tiles) * kBlock;
     u.fkb_off = nb_before * g.H + (int64_t)h * u.nb;
     u.rem_off = (int64_t)s0 * g.H + h;
     u.rem_stride = g.H;
@@ -91,6 +95,42 @@ __device__ __forceinline__ void grouped_order(int cta, int n_items, int BH, int&
   const int gsz = min(kUnitGroup, BH - grp * kUnitGroup);
   item = rem / gsz;
   unit = grp * kUnitGroup + rem % gsz;
+}
+
+// Dynamic work queue of the persistent kernels: the producer warp takes item
+// indices from a global counter (atomicAdd; items are independent, so results
+// do not depend on which CTA runs an item) and hands them to the CTA's other
+// warps through a 4-deep smem ring.  Index -1 ends the CTA's loop.
+struct SchedRing {
+  int* slot;       // [4] item indices
+  uint64_t* full;  // [4] count 1
+  uint64_t* empty; // [4] count = consumer warps
+};
+__device__ __forceinline__ void sched_init(const SchedRing& q, int consumers) {
+  for (int i = 0; i < 4; ++i) {
+    mbar_init(q.full + i, 1);
+    mbar_init(q.empty + i, consumers);
+  }
+}
+// producer warp, k-th item (whole warp; returns the index to every lane)
+__device__ __forceinline__ int sched_produce(const SchedRing& q, int k, unsigned* ctr, int n_items) {
+  int idx = 0;
+  if ((threadIdx.x & 31) == 0) {
+    idx = (int)atomicAdd(ctr, 1u);
+    if (idx >= n_items) idx = -1;
+    if (k >= 4) mbar_wait(q.empty + (k & 3), ((k >> 2) - 1) & 1);
+    q.slot[k & 3] = idx;
+    mbar_arrive(q.full + (k & 3));
+  }
+  return __shfl_sync(0xffffffffu, idx, 0);
+}
+// consumer warp, k-th item
+__device__ __forceinline__ int sched_consume(const SchedRing& q, int k) {
+  mbar_wait(q.full + (k & 3), (k >> 2) & 1);
+  const int idx = *(volatile int*)(q.slot + (k & 3));
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(q.empty + (k & 3));
+  return idx;
 }
 
 // tile(qb, kb) = qb*(qb+1)/2 + kb, the reference's (qb, kb) snapshot key order

@@ -36,6 +36,7 @@ import torch
 from . import _lib
 
 DEFAULT_BLOCK = 64
+SCHED_HEADER = 64  # floats at the start of M / N holding the kernels' work-queue counters
 SKIP_EPS_BF16 = 1e-6  # the reference's f32 default (blocked.py:43) is used for bf16
 
 
@@ -203,7 +204,7 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
     else:
         o.zero_()
         log_rem.zero_()
-    total = n_snap.value // DEFAULT_BLOCK
+    total = (n_snap.value - SCHED_HEADER) // DEFAULT_BLOCK
     visited = int(cnt[0].item()) if counters else -1
     stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
     cache = BlockedCache(q, k, v, scale, None, log_rem, first_kb, M, skip, skip_eps,
@@ -301,7 +302,7 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     _lib.check(lib.sb_bwd_phase(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
                                 _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M),
                                 _ptr(N), _ptr(dq), _ptr(dk), _ptr(dv), int(phases), _stream()))
-    n_stored = (cache.M.numel() // DEFAULT_BLOCK if cache.cu_seqlens is not None
+    n_stored = ((cache.M.numel() - SCHED_HEADER) // DEFAULT_BLOCK if cache.cu_seqlens is not None
                 else cache.layout.n_tiles * q.shape[0] * q.shape[1])
     return dq, dk, dv, n_stored
 

@@ -59,10 +59,11 @@ def _params(**kw):
 
 
 def test_snapshot_elems_matches_layout(lib):
-    # M/N: B*H*n_tiles*64 with n_tiles = nb(nb+1)/2 (blocked.py:58-60)
+    # M/N: a 64-float work-queue header + B*H*n_tiles*64 with n_tiles = nb(nb+1)/2
+    # (blocked.py:58-60)
     p = _params(B=2, H=3, L=200)
     nb = 4
-    assert lib.sb_snapshot_elems(ctypes.byref(p)) == 2 * 3 * nb * (nb + 1) // 2 * 64
+    assert lib.sb_snapshot_elems(ctypes.byref(p)) == 64 + 2 * 3 * nb * (nb + 1) // 2 * 64
 
 
 @pytest.mark.parametrize("kw,code", [
@@ -85,7 +86,7 @@ def test_varlen_elems(lib):
     snap, fkb = ctypes.c_size_t(), ctypes.c_size_t()
     assert lib.sb_varlen_elems(ctypes.byref(p), cu, ctypes.byref(snap), ctypes.byref(fkb)) == 0
     nbs = [4, 0, 2]
-    assert snap.value == 2 * sum(n * (n + 1) // 2 for n in nbs) * 64
+    assert snap.value == 64 + 2 * sum(n * (n + 1) // 2 for n in nbs) * 64
     assert fkb.value == 2 * sum(nbs)
     bad = (ctypes.c_int32 * 4)(0, 200, 100, 265)
     assert lib.sb_varlen_elems(ctypes.byref(p), bad, ctypes.byref(snap), ctypes.byref(fkb)) == 1
