@@ -169,12 +169,45 @@ struct BwdQCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kKVBytes;        // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 * 7;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 * 8 + 1 + 8;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
 };
 
+// Work item of phase 1: (unit, query-tile pair p); all roles derive the same list.
+struct QItem {
+  Unit u;
+  int b, h, p, kbhi0, kbhi1, kb_lo, n_s;
+  bool has1, valid;
+};
+__device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int idx) {
+  QItem it;
+  int item, bh;
+  grouped_order(idx, (g.n_qt + 1) / 2, g.B * g.H, item, bh);
+  it.b = bh / g.H;
+  it.h = bh % g.H;
+  it.u = make_unit(g, it.b, it.h);
+  const int n_pairs = (it.u.n_qt + 1) / 2;
+  it.valid = item < n_pairs;  // varlen: shorter sequences have fewer pairs
+  it.p = n_pairs - 1 - item;  // heaviest pairs first (longest-processing-time order)
+  it.has1 = 2 * it.p + 1 < it.u.n_qt;
+  it.kbhi0 = min(4 * it.p + 1, it.u.nb - 1);
+  it.kbhi1 = it.has1 ? min(4 * it.p + 3, it.u.nb - 1) : it.kbhi0;
+  it.kb_lo = it.kbhi1;
+  if (it.valid) {
+    const int* fkb = first_kb + it.u.fkb_off;
+    for (int qb = 4 * it.p; qb <= it.kbhi1; ++qb) it.kb_lo = min(it.kb_lo, fkb[qb]);
+  }
+  it.n_s = it.kbhi1 - it.kb_lo + 1;  // stream tiles, kb = kb_lo .. kbhi1
+  return it;
+}
+
+// Persistent: one CTA per SM takes (unit, query pair) items from a global work
+// queue.  The K ring / V buffer and each warpgroup's S, dW, dZ barriers run on
+// counters that continue across items; the next item's Q/dO load once both
+// warpgroups issued their last dW of the current item (qdo_free), and its
+// first dQ MMA waits until the warpgroup read dQ out of TMEM (dq_free).
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     sb_bwd_q_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -187,22 +220,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                              ~uintptr_t(1023));
   const Geom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heaviest pairs first (longest-processing-time order keeps the tail short)
-  const int BH = g.B * g.H;
-  int item, bh;
-  grouped_order((int)blockIdx.x, (g.n_qt + 1) / 2, BH, item, bh);
-  const int b = bh / g.H, h = bh % g.H;
-  const Unit u = make_unit(g, b, h);
-  const int n_pairs = (u.n_qt + 1) / 2;
-  if (item >= n_pairs) return;  // shorter sequence of a varlen batch: no work
-  const int p = n_pairs - 1 - item;
-  const bool has1 = 2 * p + 1 < u.n_qt;
-  const int kbhi0 = min(4 * p + 1, u.nb - 1);
-  const int kbhi1 = has1 ? min(4 * p + 3, u.nb - 1) : kbhi0;
-  const int* fkb = args.first_kb + u.fkb_off;
-  int kb_lo = kbhi1;
-  for (int qb = 4 * p; qb <= kbhi1; ++qb) kb_lo = min(kb_lo, fkb[qb]);
-  const int n_s = kbhi1 - kb_lo + 1;  // stream tiles, kb = kb_lo .. kbhi1
+  const int n_items = ((g.n_qt + 1) / 2) * g.B * g.H;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* bar_qdo = bars;
@@ -210,26 +228,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_kempty = bar_kfull + ST;
   uint64_t* bar_vfull = bar_kempty + ST;
   uint64_t* bar_vempty = bar_vfull + 1;
-  uint64_t* wgbars = bar_vempty + 1;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done
+  uint64_t* wgbars = bar_vempty + 1;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done, dq_free
+  uint64_t* bar_qdofree = wgbars + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+  const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), bar_qdofree + 1,
+                     bar_qdofree + 5};
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qdo, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_kfull + s, 1);
-      mbar_init(bar_kempty + s, has1 ? 2 : 1);  // dQ of each warpgroup read K
+      mbar_init(bar_kempty + s, 2);  // one arrival per warpgroup issuer (dQ read K)
     }
     mbar_init(bar_vfull, 1);
-    mbar_init(bar_vempty, has1 ? 2 : 1);  // dW of each warpgroup read V
+    mbar_init(bar_vempty, 2);  // one arrival per warpgroup issuer (dW read V)
     for (int w = 0; w < 2; ++w) {
-      mbar_init(wgbars + w * 7 + 0, 1);    // sfull: S = Q K^T landed in TMEM
-      mbar_init(wgbars + w * 7 + 1, 128);  // sempty: S read into registers
-      mbar_init(wgbars + w * 7 + 2, 1);    // wfull: dW = dO V^T landed
-      mbar_init(wgbars + w * 7 + 3, 128);  // wempty: dW read
-      mbar_init(wgbars + w * 7 + 4, 128);  // zfull: dZ in smem
-      mbar_init(wgbars + w * 7 + 5, 1);    // zempty: dQ MMA read dZ
-      mbar_init(wgbars + w * 7 + 6, 1);    // done
+      mbar_init(wgbars + w * 8 + 0, 1);    // sfull: S = Q K^T landed in TMEM
+      mbar_init(wgbars + w * 8 + 1, 128);  // sempty: S read into registers
+      mbar_init(wgbars + w * 8 + 2, 1);    // wfull: dW = dO V^T landed
+      mbar_init(wgbars + w * 8 + 3, 128);  // wempty: dW read
+      mbar_init(wgbars + w * 8 + 4, 128);  // zfull: dZ in smem
+      mbar_init(wgbars + w * 8 + 5, 1);    // zempty: dQ MMA read dZ
+      mbar_init(wgbars + w * 8 + 6, 1);    // done: the item's last dQ MMA completed
+      mbar_init(wgbars + w * 8 + 7, 128);  // dq_free: dQ read out of TMEM
     }
+    mbar_init(bar_qdofree, 2);
+    sched_init(sq, 10);  // consumers: stick warps 0-7, issuer warps 9-10
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -240,44 +264,67 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp >= 8) {
     reg_dealloc<kRegsLowQ>();
-  if (warp == 8) {
-    if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_do);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      const int nw = has1 ? 2 : 1;
-      mbar_expect_tx(bar_qdo, nw * 2 * C::kQBytes);
-      for (int w = 0; w < nw; ++w)
-        for (int c = 0; c < D / 64; ++c) {
-          const int row0 = (2 * p + w) * kTileM;
-          tma_load_4d(&tm_q, bar_qdo, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
-                      c * 64, u.trow0 + row0, h, u.tb);
-          tma_load_4d(&tm_do, bar_qdo, smem + C::kOffDO + w * C::kQBytes + c * (kTileM * 128),
-                      c * 64, u.trow0 + row0, h, u.tb);
-        }
-      for (int j = 0; j < n_s; ++j) {
-        const int s = j % ST;
-        if (j >= ST) mbar_wait(bar_kempty + s, ((j / ST) - 1) & 1);
-        SB_TR(args, 2, j, 12);
-        const int kb = kb_lo + j;
-        mbar_expect_tx(bar_kfull + s, C::kKVBytes);
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_4d(&tm_k, bar_kfull + s, smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128),
-                      c * 64, u.trow0 + kb * kBlock, h, u.tb);
-        if (j >= 1) mbar_wait(bar_vempty, (j - 1) & 1);
-        mbar_expect_tx(bar_vfull, C::kKVBytes);
-        for (int c = 0; c < D / 64; ++c)
-          tma_load_4d(&tm_v, bar_vfull, smem + C::kOffV + c * (kBlock * 128), c * 64,
-                      u.trow0 + kb * kBlock, h, u.tb);
+    if (warp == 8) {
+      // ---------------------------------------------------------- TMA producer
+      const bool leader = elect_one();
+      if (leader) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_do);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
       }
-    }
-  } else if (warp == 9 || warp == 10) {
-    // whole warp: uniform control flow and descriptors; one elected lane issues
-    const int w = warp - 9;
-    if (w == 0 || has1) {
-      uint64_t *sfull = wgbars + w * 7, *sempty = sfull + 1, *wfull = sfull + 2,
-               *wempty = sfull + 3, *zfull = sfull + 4, *zempty = sfull + 5, *done = sfull + 6;
+      int jg = 0, ni = 0;
+      for (int kq = 0;; ++kq) {
+        const int idx = sched_produce(sq, kq, args.sched, n_items);
+        if (idx < 0) break;
+        const QItem it = q_item(g, args.first_kb, idx);
+        if (!it.valid) continue;
+        const Unit& u = it.u;
+        if (ni >= 1) mbar_wait(bar_qdofree, (ni - 1) & 1);
+        if (leader) {
+          const int nw = it.has1 ? 2 : 1;
+          mbar_expect_tx(bar_qdo, nw * 2 * C::kQBytes);
+          for (int w = 0; w < nw; ++w)
+            for (int c = 0; c < D / 64; ++c) {
+              const int row0 = (2 * it.p + w) * kTileM;
+              tma_load_4d(&tm_q, bar_qdo, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
+                          c * 64, u.trow0 + row0, it.h, u.tb);
+              tma_load_4d(&tm_do, bar_qdo, smem + C::kOffDO + w * C::kQBytes + c * (kTileM * 128),
+                          c * 64, u.trow0 + row0, it.h, u.tb);
+            }
+        }
+        __syncwarp();
+        for (int j = 0; j < it.n_s; ++j, ++jg) {
+          const int s = jg % ST;
+          if (jg >= ST) mbar_wait(bar_kempty + s, ((jg / ST) - 1) & 1);
+          SB_TR(args, 2, jg, 12);
+          const int kb = it.kb_lo + j;
+          if (leader) {
+            mbar_expect_tx(bar_kfull + s, C::kKVBytes);
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_4d(&tm_k, bar_kfull + s,
+                          smem + C::kOffK + s * C::kKVBytes + c * (kBlock * 128), c * 64,
+                          u.trow0 + kb * kBlock, it.h, u.tb);
+          }
+          __syncwarp();
+          if (jg >= 1) mbar_wait(bar_vempty, (jg - 1) & 1);
+          if (leader) {
+            mbar_expect_tx(bar_vfull, C::kKVBytes);
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_4d(&tm_v, bar_vfull, smem + C::kOffV + c * (kBlock * 128), c * 64,
+                          u.trow0 + kb * kBlock, it.h, u.tb);
+          }
+          __syncwarp();
+        }
+        ++ni;
+      }
+    } else if (warp == 9 || warp == 10) {
+      // ---------------------------------------------------------- MMA issuer of one WG
+      // whole warp: uniform control flow and descriptors; one elected lane issues
+      const int w = warp - 9;
+      uint64_t *sfull = wgbars + w * 8, *sempty = sfull + 1, *wfull = sfull + 2,
+               *wempty = sfull + 3, *zfull = sfull + 4, *zempty = sfull + 5, *done = sfull + 6,
+               *dq_free = sfull + 7;
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T, dO V^T
       constexpr uint32_t idesc_q = idesc_bf16(128, D, 0, 1);   // dZ K: K is MN-major
       const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ + w * C::kQBytes), 16, 1024);
@@ -287,116 +334,156 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), 16, 1024);
       const uint64_t dz = sdesc_sw128(smem_u32(smem + C::kOffZ + w * C::kZBytes), 16, 1024);
       const uint32_t tS = tbase + w * 256, tW = tS + 64, tQ = tS + 128;
-      const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
       const bool leader = elect_one();
-      mbar_wait(bar_qdo, 0);
-      // Static issue order: S(j+1) once S(j) was read (it runs while the
-      // warpgroup still works on tile j), dQ(j) once dZ(j) is in smem, dW(j+1)
-      // once dW(j) was read and V(j+1) landed (V is single-buffered).
-      auto issue_s = [&](int j) {
-        const int s = j % ST;
-        mbar_wait(bar_kfull + s, (j / ST) & 1);
-        SB_TR(args, 2 + w, j, 13);
-        if (j >= 1) mbar_wait(sempty, (j - 1) & 1);
-        SB_TR(args, 2 + w, j, 8);
-        tc_fence_after();
-        if (leader) {
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-            const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-            umma_ss_at(tS, dq, off, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
+      int jg = 0, ni = 0, ig = 0, nwi = 0;
+      for (int kq = 0;; ++kq) {
+        const int idx = sched_consume(sq, kq);
+        if (idx < 0) break;
+        const QItem it = q_item(g, args.first_kb, idx);
+        if (!it.valid) continue;
+        if (w == 1 && !it.has1) {  // no tile for this warpgroup: release the stream
+          for (int j = 0; j < it.n_s; ++j) {
+            const int js = jg + j;
+            mbar_wait(bar_kfull + js % ST, (js / ST) & 1);
+            if (leader) mbar_arrive(bar_kempty + js % ST);
+            mbar_wait(bar_vfull, js & 1);
+            if (leader) mbar_arrive(bar_vempty);
+            __syncwarp();
           }
-          umma_commit(sfull);
+          // (after a K of this item landed: the producer is past the previous
+          // item's qdo_free phase, so this arrival counts for this item's phase)
+          if (leader) mbar_arrive(bar_qdofree);
+          __syncwarp();
+          jg += it.n_s;
+          ++ni;
+          continue;
         }
-        __syncwarp();
-      };
-      auto issue_w = [&](int j) {
-        mbar_wait(bar_vfull, j & 1);
-        if (j >= 1) mbar_wait(wempty, (j - 1) & 1);
-        SB_TR(args, 2 + w, j, 10);
-        tc_fence_after();
-        if (leader) {
+        const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
+        mbar_wait(bar_qdo, ni & 1);
+        // Static issue order: S(j+1) once S(j) was read (it runs while the
+        // warpgroup still works on tile j), dQ(j) once dZ(j) is in smem, dW(j+1)
+        // once dW(j) was read and V(j+1) landed (V is single-buffered).
+        auto issue_s = [&](int j) {
+          const int js = jg + j, s = js % ST, gi = ig + j;
+          mbar_wait(bar_kfull + s, (js / ST) & 1);
+          SB_TR(args, 2 + w, gi, 13);
+          if (gi >= 1) mbar_wait(sempty, (gi - 1) & 1);
+          SB_TR(args, 2 + w, gi, 8);
+          tc_fence_after();
+          if (leader) {
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
-            const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-            umma_ss_at(tW, ddo, off, dv, offk, idesc_s, k > 0);
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+              umma_ss_at(tS, dq, off, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
+            }
+            umma_commit(sfull);
           }
-          umma_commit(wfull);
-          umma_commit(bar_vempty);
-        }
-        __syncwarp();
-      };
-      issue_s(0);
-      issue_w(0);
-      for (int j = 0; j < n_w; ++j) {
-        if (j + 1 < n_w) issue_s(j + 1);
-        const int s = j % ST;
-        mbar_wait(zfull, j & 1);
-        SB_TR(args, 2 + w, j, 11);
-        tc_fence_after();
-        if (leader) {
+          __syncwarp();
+        };
+        auto issue_w = [&](int j) {
+          const int js = jg + j, gi = ig + j;
+          mbar_wait(bar_vfull, js & 1);
+          if (gi >= 1) mbar_wait(wempty, (gi - 1) & 1);
+          SB_TR(args, 2 + w, gi, 10);
+          tc_fence_after();
+          if (leader) {
 #pragma unroll
-          for (int k = 0; k < kBlock / 16; ++k)
-            umma_ss_at(tQ, dz, k * 32, dkmn, s * C::kKVBytes + k * 2048, idesc_q,
-                    (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(zempty);
-          umma_commit(bar_kempty + s);
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+              const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
+              umma_ss_at(tW, ddo, off, dv, offk, idesc_s, k > 0);
+            }
+            umma_commit(wfull);
+            umma_commit(bar_vempty);
+            if (j + 1 == n_w) umma_commit(bar_qdofree);  // Q and dO read for the last time
+          }
+          __syncwarp();
+        };
+        issue_s(0);
+        issue_w(0);
+        for (int j = 0; j < n_w; ++j) {
+          if (j + 1 < n_w) issue_s(j + 1);
+          const int js = jg + j, s = js % ST, gi = ig + j;
+          mbar_wait(zfull, gi & 1);
+          SB_TR(args, 2 + w, gi, 11);
+          // the previous item's dQ must be out of TMEM before it is overwritten
+          if (j == 0 && nwi >= 1) mbar_wait(dq_free, (nwi - 1) & 1);
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
+            for (int k = 0; k < kBlock / 16; ++k)
+              umma_ss_at(tQ, dz, k * 32, dkmn, s * C::kKVBytes + k * 2048, idesc_q,
+                         (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(zempty);
+            umma_commit(bar_kempty + s);
+            if (j + 1 == n_w) umma_commit(done);
+          }
+          __syncwarp();
+          if (j + 1 < n_w) issue_w(j + 1);
         }
-        __syncwarp();
-        if (j + 1 < n_w) issue_w(j + 1);
-      }
-      if (leader) umma_commit(done);
-      __syncwarp();
-      for (int j = n_w; j < n_s; ++j) {  // stream tiles right of this WG's diagonal
-        // release each buffer in its own phase: wait until tile j occupies it
-        mbar_wait(bar_kfull + j % ST, (j / ST) & 1);
-        if (leader) mbar_arrive(bar_kempty + j % ST);
-        mbar_wait(bar_vfull, j & 1);
-        if (leader) mbar_arrive(bar_vempty);
-        __syncwarp();
+        for (int j = n_w; j < it.n_s; ++j) {  // stream tiles right of this WG's diagonal
+          // release each buffer in its own phase: wait until tile j occupies it
+          const int js = jg + j;
+          mbar_wait(bar_kfull + js % ST, (js / ST) & 1);
+          if (leader) mbar_arrive(bar_kempty + js % ST);
+          mbar_wait(bar_vfull, js & 1);
+          if (leader) mbar_arrive(bar_vempty);
+          __syncwarp();
+        }
+        jg += it.n_s;
+        ig += n_w;
+        ++ni;
+        ++nwi;
       }
     }
-  }
   } else {
     reg_alloc<kRegsHighQ>();
+    // ------------------------------------------------------------ stick warpgroups
     const int w = warp >> 2;
-    if (w == 0 || has1) {
-      uint64_t *sfull = wgbars + w * 7, *sempty = sfull + 1, *wfull = sfull + 2,
-               *wempty = sfull + 3, *zfull = sfull + 4, *zempty = sfull + 5, *done = sfull + 6;
-      const int quarter = warp & 3;
-      const int r = quarter * 32 + lane;
-      const int qt = 2 * p + w;
+    uint64_t *sfull = wgbars + w * 8, *sempty = sfull + 1, *wfull = sfull + 2,
+             *wempty = sfull + 3, *zfull = sfull + 4, *zempty = sfull + 5, *done = sfull + 6,
+             *dq_free = sfull + 7;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tbase + w * 256 + lane_base, tW = tS + 64, tQ = tS + 128;
+    const uint32_t z_row = smem_u32(smem + C::kOffZ + w * C::kZBytes) + r * 128;
+    const float scale = g.scale_log2 * kLn2;
+    const bool tr = quarter == 0 && lane == 0;
+    if (tr) SB_TR(args, w, 0, 14);
+    int ig = 0, nwi = 0;
+    for (int kq = 0;; ++kq) {
+      const int idx = sched_consume(sq, kq);
+      if (idx < 0) break;
+      const QItem it = q_item(g, args.first_kb, idx);
+      if (!it.valid || (w == 1 && !it.has1)) continue;
+      const Unit& u = it.u;
+      const int qt = 2 * it.p + w;
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
       const bool row_valid = row < u.L;
       const bool half_exists = my_qb < u.nb;
-      const int my_first = half_exists ? fkb[my_qb] : u.nb;
-      const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-      const uint32_t tS = tbase + w * 256 + lane_base, tW = tS + 64, tQ = tS + 128;
+      const int my_first = half_exists ? args.first_kb[u.fkb_off + my_qb] : u.nb;
       const float off =
           (args.row_offset && row_valid) ? args.row_offset[u.rem_off + row * u.rem_stride] : 0.0f;
       const float* Mrow = args.M + u.m_off + (r & 63);
       float* Nrow = args.N + u.m_off + (r & 63);
-      const uint32_t z_row = smem_u32(smem + C::kOffZ + w * C::kZBytes) + r * 128;
-      const int n_w = (w ? kbhi1 : kbhi0) - kb_lo + 1;
+      const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
       auto tile_of = [&](int kb) -> int64_t {  // snapshot slot (row 0 of the unit if not live)
         const bool lv = row_valid && kb >= my_first && kb <= my_qb;
         return tile_index(lv ? my_qb : 0, lv ? kb : 0) * kBlock;
       };
-      float Ma = Mrow[tile_of(kb_lo)];  // M of the next tile, loaded one tile ahead
-      float bsum = 0.0f;  // running b (blocked.py:342, :354)
-      const bool tr = quarter == 0 && lane == 0;
-      if (tr) SB_TR(args, w, 0, 14);
+      float Ma = Mrow[tile_of(it.kb_lo)];  // M of the next tile, loaded one tile ahead
+      float bsum = 0.0f;                   // running b (blocked.py:342, :354)
       for (int j = 0; j < n_w; ++j) {
-        const int kb = kb_lo + j;
+        const int kb = it.kb_lo + j, gi = ig + j;
         const bool live = row_valid && kb >= my_first && kb <= my_qb;
         const int64_t t = tile_of(kb);
         const float E = live ? ex2(Ma) : 0.0f;
         if (j + 1 < n_w) Ma = Mrow[tile_of(kb + 1)];
-        if (tr) SB_TR(args, w, j, 0);
-        mbar_wait(sfull, j & 1);
+        if (tr) SB_TR(args, w, gi, 0);
+        mbar_wait(sfull, gi & 1);
         tc_fence_after();
         float s[64], sg[64];
         tmem_ld32(tS, s);
@@ -404,35 +491,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
-        if (tr) SB_TR(args, w, j, 1);
+        if (tr) SB_TR(args, w, gi, 1);
         const bool diag = kb == my_qb;  // warp-uniform
         // dead rows/tiles run the same code with e^M = 0 and b = 0: A = 0, dZ = 0
         if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
         else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
-        if (tr) SB_TR(args, w, j, 2);
-        mbar_wait(wfull, j & 1);
+        if (tr) SB_TR(args, w, gi, 2);
+        mbar_wait(wfull, gi & 1);
         tc_fence_after();
         if (args.row_offset) load_dat<true>(s, tW, off);
         else load_dat<false>(s, tW, off);
         tc_fence_before();
         mbar_arrive(wempty);
-        if (tr) SB_TR(args, w, j, 3);
+        if (tr) SB_TR(args, w, gi, 3);
         uint32_t pk[32];
         if (live) Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
         const float bnext = dz_row(s, sg, live ? bsum : 0.0f, pk);
         bsum = live ? bnext : bsum;
-        if (tr) SB_TR(args, w, j, 4);
-        if (j >= 1) mbar_wait(zempty, (j - 1) & 1);
-        if (tr) SB_TR(args, w, j, 5);
+        if (tr) SB_TR(args, w, gi, 4);
+        if (gi >= 1) mbar_wait(zempty, (gi - 1) & 1);
+        if (tr) SB_TR(args, w, gi, 5);
         store_row_sw128(z_row, r, pk);
         fence_proxy_async_smem();
         mbar_arrive(zfull);
-        if (tr) SB_TR(args, w, j, 6);
+        if (tr) SB_TR(args, w, gi, 6);
       }
-      mbar_wait(done, 0);
+      mbar_wait(done, nwi & 1);
       if (tr) SB_TR(args, w, 0, 15);
       tc_fence_after();
-      const float scale = g.scale_log2 * kLn2;
       // dQ rows leave in 64-column halves through this warp's 4 KB slice of the
       // (now idle: `done`) dZ buffer as coalesced row segments
       const int row0 = qt * kTileM + quarter * 32;
@@ -444,9 +530,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld32(tQ + c * 64, v);
         tmem_ld32(tQ + c * 64 + 32, v + 32);
         tmem_wait_ld();
+        if (c + 1 == D / 64) {
+          tc_fence_before();
+          mbar_arrive(dq_free);  // the next item's dQ may overwrite TMEM
+        }
         warp_store_rows<8>(v, scale, stage, args.dq + u.out_off + (int64_t)row0 * g.sl + c * 64,
                            g.sl, nvalid);
       }
+      ig += n_w;
+      ++nwi;
     }
   }
   tc_fence_before();
@@ -937,8 +1029,13 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
     if ((e = cudaMemsetAsync(a.sched, 0, sizeof(unsigned), stream)) != cudaSuccess) return (int)e;
-    kern<<<(unsigned)((a.g.n_qt + 1) / 2) * BH, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tv,
-                                                                                  a);
+    // persistent: one CTA per SM (fewer if there are fewer work items)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned items = (unsigned)((a.g.n_qt + 1) / 2) * BH;
+    kern<<<items < (unsigned)sms ? items : (unsigned)sms, kBwdThreads, C::kSmem, stream>>>(
+        tq, tdo, tk, tv, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   }
   if (phases & 2) {
