@@ -32,10 +32,12 @@ struct FwdPPCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffP = kOffV + kStages * kKVBytes;       // P[wg][buf]
   static constexpr int kOffBar = kOffP + 4 * kPBytes;
-  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 8 + 2 + 2 + 1 + 8;
+  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 8 + 2 + 2 + 1 + 8 + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
-  static constexpr uint32_t kTmemCols = 512;  // S[wg][2] at wg*128 + b*64, O[wg] at 256 + wg*128
+  // per WG w: S at w*128 (single-buffered), Q (MMA A operand) at w*128 + 64,
+  // O at 256 + w*128
+  static constexpr uint32_t kTmemCols = 512;
 };
 
 // Work item: (unit, query-tile pair p); all roles derive the same list.
@@ -91,6 +93,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   uint64_t* bar_qfree = bar_ofree + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), bar_qfree + 1, bar_qfree + 5};
+  uint64_t* bar_qtm = bar_qfree + 9;  // [2] the warpgroup copied its Q tile into TMEM
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
@@ -111,6 +114,8 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       mbar_init(bar_ofree + w, 128);
     }
     mbar_init(bar_qfree, 2);
+    mbar_init(bar_qtm, 128);
+    mbar_init(bar_qtm + 1, 128);
     sched_init(sq, 10);  // consumers: stick warps 0-7, issuer warps 9-10
     fence_mbar_init();
   }
@@ -173,11 +178,10 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     uint64_t* pempty = sfull + 6;
     constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T: both K-major
     constexpr uint32_t idesc_o = idesc_bf16(128, D, 0, 1);   // A V: V is MN-major
-    const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ + w * C::kQBytes), 16, 1024);
     const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
     const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), kBlock * 128, 1024);
     const uint64_t dp = sdesc_sw128(smem_u32(smem + C::kOffP + w * 2 * C::kPBytes), 16, 1024);
-    const uint32_t tS = tbase + w * 128, tO = tbase + 256 + w * 128;
+    const uint32_t tS = tbase + w * 128, tQ = tS + 64, tO = tbase + 256 + w * 128;
     const bool leader = elect_one();
     int jg = 0, ni = 0, ig = 0, nwi = 0;
     for (int k = 0;; ++k) {
@@ -202,7 +206,11 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       }
       const int j0 = it.kbhi1 - (w ? it.kbhi1 : it.kbhi0);  // first stream tile of this WG
       const int n_w = it.n_s - j0;
-      mbar_wait(bar_q, ni & 1);
+      // S = Q K^T reads Q from TMEM (copied there by the warpgroup); the smem Q
+      // buffer of this warpgroup is free for the next item from then on
+      mbar_wait(bar_qtm + w, nwi & 1);
+      if (leader) mbar_arrive(bar_qfree);
+      __syncwarp();
       auto issue_pv = [&](int i) {  // local tile i == stream tile j0 + i
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
         mbar_wait(pfull + (gi & 1), (gi >> 1) & 1);
@@ -231,18 +239,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       for (int i = 0; i < n_w; ++i) {
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
         mbar_wait(bar_kfull + s, (js / ST) & 1);
-        if (gi >= 2) mbar_wait(sempty + (gi & 1), ((gi >> 1) + 1) & 1);
+        if (gi >= 1) mbar_wait(sempty, (gi - 1) & 1);  // S is single-buffered
         SB_TR(args, 2 + w, gi, 8);
         tc_fence_after();
         if (leader) {
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
             const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-            umma_ss_at(tS + (gi & 1) * 64, dq, off, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
+            umma_ts_at(tS, tQ + k * 8, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
           }
-          umma_commit(sfull + (gi & 1));
-          if (i + 1 == n_w) umma_commit(bar_qfree);  // this item's Q was read for the last time
+          umma_commit(sfull);
         }
         __syncwarp();
         SB_TR(args, 2 + w, gi, 10);
@@ -266,18 +272,41 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t tS = tbase + w * 128 + lane_base, tO = tbase + 256 + w * 128 + lane_base;
+    const uint32_t tS = tbase + w * 128 + lane_base, tQ = tS + 64,
+                   tO = tbase + 256 + w * 128 + lane_base;
     const uint32_t p_row = smem_u32(smem + C::kOffP + w * 2 * C::kPBytes) + r * 128;
     const float sl2 = g.scale_log2;
     const bool tr = quarter == 0 && lane == 0;
     if (tr) SB_TR(args, w, 0, 14);
-    int ig = 0, nwi = 0;
+    int ig = 0, nwi = 0, ni = 0;
     for (int k = 0;; ++k) {
       const int idx = sched_consume(sq, k);
       if (idx < 0) break;
       const FwdItem it = fwd_item(g, idx);
-      if (!it.valid || (w == 1 && !it.has1)) continue;
+      if (!it.valid) continue;
+      ++ni;
+      if (w == 1 && !it.has1) continue;
       const Unit& u = it.u;
+      {
+        // copy this thread's Q row (TMA-swizzled smem) into TMEM lane r: the A
+        // operand of S = Q K^T, two bf16 of d per 32-bit column
+        mbar_wait(bar_q, (ni - 1) & 1);
+        const uint32_t qrow = smem_u32(smem + C::kOffQ + w * C::kQBytes) + r * 128;
+        uint32_t qv[D / 2];
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+          const uint4 x = ld_shared_v4(qrow + (c >> 3) * (kTileM * 128) + (((c & 7) ^ (r & 7)) << 4));
+          qv[4 * c] = x.x;
+          qv[4 * c + 1] = x.y;
+          qv[4 * c + 2] = x.z;
+          qv[4 * c + 3] = x.w;
+        }
+        if constexpr (D == 128) tmem_st64(tQ, qv);
+        else tmem_st32(tQ, qv);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar_qtm + w);
+      }
       const int qt = 2 * it.p + w;
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
@@ -289,11 +318,11 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       for (int i = 0; i < n_w; ++i) {
         const int kb = kbhi - i, gi = ig + i;
         if (tr) SB_TR(args, w, gi, 0);
-        mbar_wait(sfull + (gi & 1), (gi >> 1) & 1);
+        mbar_wait(sfull, gi & 1);
         tc_fence_after();
         float s[64];
-        tmem_ld32(tS + (gi & 1) * 64, s);
-        tmem_ld32(tS + (gi & 1) * 64 + 32, s + 32);
+        tmem_ld32(tS, s);
+        tmem_ld32(tS + 32, s + 32);
         tmem_wait_ld();
         if (tr) SB_TR(args, w, gi, 1);
         uint32_t pk[32];
@@ -314,8 +343,8 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         if (__any_sync(0xffffffffu, slow)) {
           // a group product of (1+t) reached 2^64: per-element path for those rows
           // (S is still in TMEM: s_empty not yet signalled)
-          tmem_ld32(tS + (gi & 1) * 64, s);
-          tmem_ld32(tS + (gi & 1) * 64 + 32, s + 32);
+          tmem_ld32(tS, s);
+          tmem_ld32(tS + 32, s + 32);
           tmem_wait_ld();
           if (slow) {
             // per-element product form for A, exact softplus sum for a
@@ -341,7 +370,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(sempty + (gi & 1));
+        mbar_arrive(sempty);  // S(i+1) may overwrite the buffer now
         if (tr) SB_TR(args, w, gi, 2);
         if (gi >= 2) mbar_wait(pempty + (gi & 1), ((gi >> 1) + 1) & 1);
         if (tr) SB_TR(args, w, gi, 3);
