@@ -206,16 +206,24 @@ def main():
         if ev is not None:
             ev[1].record(stream)
         out = step.out
-        sb.blocked_backward_twophase(cache, d_o, out=out, phases=1)
+        sb.blocked_backward_twophase(cache, d_o, out=out, phases=1, tiles=step.tiles,
+                                     store_tiles=step.tiles is not None)
         if ev is not None:
             ev[2].record(stream)
-        sb.blocked_backward_twophase(cache, d_o, out=out, phases=2)
+        sb.blocked_backward_twophase(cache, d_o, out=out, phases=2, tiles=step.tiles,
+                                     store_tiles=step.tiles is not None)
         return o
 
     M_elems = sb.ops._lib.load().sb_snapshot_elems(
         __import__("ctypes").byref(sb.ops._params(q, 1.0 / math.sqrt(D), False, 1e-6)))
     step.out = (torch.empty(M_elems, device=dev, dtype=torch.float32), torch.empty_like(q),
                 torch.empty_like(q), torch.empty_like(q))
+    # dZ tile workspace of the store-mode backward (shared by the two phase launches)
+    _, _, _, cache0 = sb.blocked_forward(q, k, v, counters=False)
+    n_tiles_bytes = sb.ops.tile_workspace_bytes(cache0)
+    step.tiles = (torch.empty(n_tiles_bytes, device=dev, dtype=torch.uint8)
+                  if n_tiles_bytes <= sb.ops.TILE_WORKSPACE_MAX_BYTES else None)
+    del cache0
 
     for _ in range(W):
         step()

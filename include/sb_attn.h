@@ -15,6 +15,8 @@
  *   sb_bwd       blocked.py:299  blocked_backward_twophase(cache, d_o, layout,
  *                                row_offset)     -> (d_q, d_k, d_v, n_stored)
  *   sb_bwd_phase blocked.py:337-357 / :367-386, the two phases of sb_bwd
+ *   sb_bwd_ws    sb_bwd_phase with the dZ tile workspace (store mode: phase 2 reads
+ *                phase 1's dZ instead of recomputing it; same results)
  *   sb_snapshot_elems  blocked.py:58-60 BlockLayout.n_tiles x d_block (M/N size)
  *   sb_varlen_elems    the same sizes for a packed variable-length batch (each
  *                      sequence planned separately)
@@ -102,6 +104,20 @@ int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void*
                  const void* d_o, const float* row_offset, const float* log_rem,
                  const int32_t* first_kb, const float* M, float* N, void* dq, void* dk, void* dv,
                  int phases, void* stream);
+
+/* Store mode of the backward.  Bytes of the dZ tile workspace: phase 1 writes
+ * every 128-row x 64-key dZ tile it computes (bf16, 16 KB each; per (b,h) unit
+ * n_qt*(n_qt+1) tiles, n_qt = ceil(L/128)) and phase 2 reads them back instead of
+ * recomputing dO.V^T and dZ (same results, bit for bit).  cu_seqlens_host: host
+ * copy of the offsets for packed varlen batches, else NULL. */
+size_t sb_bwd_tile_bytes(const sb_params_t* p, const int32_t* cu_seqlens_host);
+
+/* sb_bwd_phase with an optional dZ tile workspace (ztiles: device, 128-byte
+ * aligned, ztiles_bytes >= sb_bwd_tile_bytes; NULL = recompute mode). */
+int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
+              const float* row_offset, const float* log_rem, const int32_t* first_kb,
+              const float* M, float* N, void* dq, void* dk, void* dv, void* ztiles,
+              size_t ztiles_bytes, int phases, void* stream);
 
 const char* sb_status_string(int status);
 int sb_version(void);

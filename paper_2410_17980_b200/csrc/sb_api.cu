@@ -53,6 +53,21 @@ int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
   return r == CUDA_SUCCESS ? SB_OK : SB_ERR_LAUNCH;
 }
 
+// 3-D map over the dZ tile workspace: 64 bf16 columns x 128 rows x n_tiles, the
+// 128B-swizzled smem image of a tile (store mode of the backward).
+int make_tile_map(CUtensorMap* m, void* ptr, size_t bytes) {
+  auto fn = encode_fn();
+  if (!fn) return SB_ERR_DEVICE;
+  const cuuint64_t dims[3] = {64, 128, (cuuint64_t)(bytes / sb::kZTileBytes)};
+  const cuuint64_t strides[2] = {128, (cuuint64_t)sb::kZTileBytes};
+  const cuuint32_t box[3] = {64, 128, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SB_OK : SB_ERR_LAUNCH;
+}
+
 int validate(const sb_params_t* p) {
   if (!p) return SB_ERR_NULL;
   if (p->cu_seqlens && p->total_tokens < 1) return SB_ERR_SHAPE;
@@ -152,10 +167,34 @@ int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, co
   return sb_bwd_phase(p, q, k, v, d_o, row_offset, log_rem, first_kb, M, N, dq, dk, dv, 3, stream);
 }
 
+size_t sb_bwd_tile_bytes(const sb_params_t* p, const int32_t* cu) {
+  if (!p || p->seqlen < 1) return 0;
+  size_t tiles = 0;
+  if (!p->cu_seqlens) {
+    const size_t nq = (size_t)(p->seqlen + 127) / 128;
+    tiles = (size_t)p->batch * p->heads * nq * (nq + 1);
+  } else {
+    if (!cu) return 0;
+    for (int b = 0; b < p->batch; ++b) {
+      const size_t nq = (size_t)(cu[b + 1] - cu[b] + 127) / 128;
+      tiles += (size_t)p->heads * nq * (nq + 1);
+    }
+  }
+  return tiles * sb::kZTileBytes;
+}
+
 int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void* v,
                  const void* d_o, const float* row_offset, const float* log_rem,
                  const int32_t* first_kb, const float* M, float* N, void* dq, void* dk, void* dv,
                  int phases, void* stream) {
+  return sb_bwd_ws(p, q, k, v, d_o, row_offset, log_rem, first_kb, M, N, dq, dk, dv, nullptr, 0,
+                   phases, stream);
+}
+
+int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
+              const float* row_offset, const float* log_rem, const int32_t* first_kb,
+              const float* M, float* N, void* dq, void* dk, void* dv, void* ztiles,
+              size_t ztiles_bytes, int phases, void* stream) {
   if (phases < 1 || phases > 3) return SB_ERR_SHAPE;
   int st = validate(p);
   if (st) return st;
@@ -165,10 +204,17 @@ int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void*
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(d_o) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return SB_ERR_UNSUPPORTED;
-  CUtensorMap tq, tdo, tk, tv;
+  CUtensorMap tq, tdo, tk, tv, tz;
   if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
       (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)))
     return st;
+  const bool store = ztiles != nullptr;
+  std::memset(&tz, 0, sizeof(tz));
+  if (store) {
+    if (ztiles_bytes < sb_bwd_tile_bytes(p, nullptr) && !p->cu_seqlens) return SB_ERR_SHAPE;
+    if (reinterpret_cast<uintptr_t>(ztiles) & 127) return SB_ERR_UNSUPPORTED;
+    if ((st = make_tile_map(&tz, ztiles, ztiles_bytes))) return st;
+  }
   sb::BwdArgs a;
   a.g = geom(p);
   a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
@@ -180,7 +226,7 @@ int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void*
   a.N = N;
   a.trace = g_trace;
   a.sched = reinterpret_cast<unsigned*>(N);
-  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, a, phases,
+  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, a, phases, store,
                             reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
@@ -200,7 +246,7 @@ const char* sb_status_string(int s) {
   }
 }
 
-int sb_version(void) { return 2; }  // 2: packed varlen (cu_seqlens, total_tokens)
+int sb_version(void) { return 3; }  // 2: packed varlen; 3: dZ tile workspace (sb_bwd_ws)
 
 #ifdef SB_TRACE
 // debug builds only: device buffer of kTraceCtas*4*64*16 uint32 clock stamps

@@ -48,7 +48,8 @@ static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "
 // scheduler can interleave them: 6 FP32 ops + 1 ex2 per element.  A row whose
 // group product reaches 2^64 (large logits; t = inf included) falls back to one
 // rcp per element.
-template <bool kDiag>
+// kSigma = false (store-mode phase 2): A only; sg[] is scratch.
+template <bool kDiag, bool kSigma = true>
 __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float E,
                                               int lim) {
 #ifdef SB_NOMATH  // tuning ablation: pipeline without the stick math
@@ -90,9 +91,9 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
         const int c = 16 * g + i;
         const float t = s[c];
         const float u = i ? t * sg[c - 1] : t;
-        sg[c] = u * inv[g];
+        if (kSigma) sg[c] = u * inv[g];
         s[c] = u * K[g];
-        inv[g] = fmaf(inv[g], t, inv[g]);
+        if (kSigma) inv[g] = fmaf(inv[g], t, inv[g]);
       }
   } else {
     float Q = E;
@@ -181,7 +182,8 @@ struct QItem {
   int b, h, p, kbhi0, kbhi1, kb_lo, n_s;
   bool has1, valid;
 };
-__device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int idx) {
+__device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int idx,
+                                        bool even_lo = false) {
   QItem it;
   int item, bh;
   grouped_order(idx, (g.n_qt + 1) / 2, g.B * g.H, item, bh);
@@ -198,6 +200,9 @@ __device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int 
   if (it.valid) {
     const int* fkb = first_kb + it.u.fkb_off;
     for (int qb = 4 * it.p; qb <= it.kbhi1; ++qb) it.kb_lo = min(it.kb_lo, fkb[qb]);
+    // store mode: start at an even key block so every key pair phase 2 loads has
+    // both of its tiles written (the extra tile is all dead rows: dZ = 0)
+    if (even_lo) it.kb_lo &= ~1;
   }
   it.n_s = it.kbhi1 - it.kb_lo + 1;  // stream tiles, kb = kb_lo .. kbhi1
   return it;
@@ -208,11 +213,13 @@ __device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int 
 // counters that continue across items; the next item's Q/dO load once both
 // warpgroups issued their last dW of the current item (qdo_free), and its
 // first dQ MMA waits until the warpgroup read dQ out of TMEM (dq_free).
-template <int D>
+// kStoreZ (store mode): each dZ tile also goes to the tile workspace (TMA store
+// from the swizzled smem buffer, issued with the dQ MMA) for phase 2 to reuse.
+template <int D, bool kStoreZ>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     sb_bwd_q_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                    const BwdArgs args) {
+                    const __grid_constant__ CUtensorMap tm_z, const BwdArgs args) {
   using C = BwdQCfg<D>;
   constexpr int ST = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -248,7 +255,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(wgbars + w * 8 + 2, 1);    // wfull: dW = dO V^T landed
       mbar_init(wgbars + w * 8 + 3, 128);  // wempty: dW read
       mbar_init(wgbars + w * 8 + 4, 128);  // zfull: dZ in smem
-      mbar_init(wgbars + w * 8 + 5, 1);    // zempty: dQ MMA read dZ
+      mbar_init(wgbars + w * 8 + 5, kStoreZ ? 2 : 1);  // zempty: dQ MMA (+ tile store) read dZ
       mbar_init(wgbars + w * 8 + 6, 1);    // done: the item's last dQ MMA completed
       mbar_init(wgbars + w * 8 + 7, 128);  // dq_free: dQ read out of TMEM
     }
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int kq = 0;; ++kq) {
         const int idx = sched_produce(sq, kq, args.sched, n_items);
         if (idx < 0) break;
-        const QItem it = q_item(g, args.first_kb, idx);
+        const QItem it = q_item(g, args.first_kb, idx, kStoreZ);
         if (!it.valid) continue;
         const Unit& u = it.u;
         if (ni >= 1) mbar_wait(bar_qdofree, (ni - 1) & 1);
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int kq = 0;; ++kq) {
         const int idx = sched_consume(sq, kq);
         if (idx < 0) break;
-        const QItem it = q_item(g, args.first_kb, idx);
+        const QItem it = q_item(g, args.first_kb, idx, kStoreZ);
         if (!it.valid) continue;
         if (w == 1 && !it.has1) {  // no tile for this warpgroup: release the stream
           for (int j = 0; j < it.n_s; ++j) {
@@ -418,9 +425,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             umma_commit(zempty);
             umma_commit(bar_kempty + s);
             if (j + 1 == n_w) umma_commit(done);
+            if (kStoreZ) {  // dZ(j) -> tile workspace
+              tma_store_3d(&tm_z, smem + C::kOffZ + w * C::kZBytes, 0, 0,
+                           (int)(it.u.z_off + ztile(2 * it.p + w, it.kb_lo + j)));
+              bulk_commit();
+            }
           }
           __syncwarp();
           if (j + 1 < n_w) issue_w(j + 1);
+          if (kStoreZ) {  // the store has read the buffer: second arrival on zempty
+            if (leader) {
+              bulk_wait_read0();
+              mbar_arrive(zempty);
+            }
+            __syncwarp();
+          }
         }
         for (int j = n_w; j < it.n_s; ++j) {  // stream tiles right of this WG's diagonal
           // release each buffer in its own phase: wait until tile j occupies it
@@ -436,6 +455,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ++ni;
         ++nwi;
       }
+      // the dZ tile stores must have reached global memory before the CTA exits
+      if (kStoreZ && leader) bulk_wait0();
+      __syncwarp();
     }
   } else {
     reg_alloc<kRegsHighQ>();
@@ -456,7 +478,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int kq = 0;; ++kq) {
       const int idx = sched_consume(sq, kq);
       if (idx < 0) break;
-      const QItem it = q_item(g, args.first_kb, idx);
+      const QItem it = q_item(g, args.first_kb, idx, kStoreZ);
       if (!it.valid || (w == 1 && !it.has1)) continue;
       const Unit& u = it.u;
       const int qt = 2 * it.p + w;
@@ -517,6 +539,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (tr) SB_TR(args, w, gi, 6);
       }
       mbar_wait(done, nwi & 1);
+      // store mode: the last tile's TMA store must have read the buffer too
+      if (kStoreZ) mbar_wait(zempty, (ig + n_w - 1) & 1);
       if (tr) SB_TR(args, w, 0, 15);
       tc_fence_after();
       // dQ rows leave in 64-column halves through this warp's 4 KB slice of the
@@ -1023,50 +1047,390 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 8) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
+// ============================================================================
+// Phase 2, store mode: dZ tiles come from the workspace phase 1 wrote, so a
+// key pair's tile needs only S = Q [K0;K1]^T and A (no dO V^T, no dZ math):
+//   dV += [A0 A1]^T dO, dK += [dZ0 dZ1]^T Q  (dZ TMA-loaded).
+// Tensor-pipe order per tile j: S(j+1) (double-buffered in TMEM, runs while the
+// warpgroups compute A(j)), dV(j), dK(j).  Q has 3 stages (S(j+1) and dK(j)
+// hold two; the third is in flight), dO and dZ one each; three producer warps
+// (K+Q, dZ, dO) refill each buffer the moment the MMA reading it completes.
+template <int D>
+struct BwdKVSCfg {
+  static constexpr int kStages = 3;                       // Q ring
+  static constexpr int kQBytes = kTileM * D * 2;
+  static constexpr int kPairBytes = 2 * kBlock * D * 2;  // K of both key blocks
+  static constexpr int kPBytes = kTileM * kBlock * 2;    // A / dZ of one key block
+  static constexpr int kOffK = 0;
+  static constexpr int kOffQ = kOffK + kPairBytes;
+  static constexpr int kOffDO = kOffQ + kStages * kQBytes;  // single buffer (free after dV)
+  static constexpr int kOffA = kOffDO + kQBytes;            // key block 0 then 1
+  static constexpr int kOffZ = kOffA + 2 * kPBytes;         // dZ of key block 0 then 1
+  static constexpr int kOffBar = kOffZ + 2 * kPBytes;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 9;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
+  static constexpr int kSmem = kOffMisc + 64 + 1024;
+  static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
+  static constexpr uint32_t kTmemCols = 512;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    sb_bwd_kvs_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_z,
+                      const BwdArgs args) {
+  using C = BwdKVSCfg<D>;
+  constexpr int ST = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const Geom& g = args.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = ((g.nb + 1) / 2) * g.B * g.H;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* bar_kv = bars;
+  uint64_t* bar_qfull = bars + 1;
+  uint64_t* bar_qempty = bar_qfull + ST;
+  uint64_t* bar_dofull = bar_qempty + ST;
+  uint64_t* bar_doempty = bar_dofull + 1;
+  uint64_t* bar_zfull = bar_doempty + 1;  // dZ pair landed
+  uint64_t* bar_zempty = bar_zfull + 1;   // dK read it
+  uint64_t* sfull = bar_zempty + 1;  // [2] S double-buffered in TMEM (cols 0 / 128)
+  uint64_t* sempty = sfull + 2;      // [2]
+  uint64_t* afull = sfull + 4;
+  uint64_t* aused = sfull + 5;
+  uint64_t* done = sfull + 6;
+  uint64_t* kv_free = sfull + 7;
+  uint64_t* acc_free = sfull + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(bar_qfull + s, 1);
+      mbar_init(bar_qempty + s, 1);
+    }
+    mbar_init(bar_dofull, 1);
+    mbar_init(bar_doempty, 1);
+    mbar_init(bar_zfull, 1);
+    mbar_init(bar_zempty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(sfull + s, 1);
+      mbar_init(sempty + s, 256);
+    }
+    mbar_init(afull, 256);
+    mbar_init(aused, 1);
+    mbar_init(done, 1);
+    mbar_init(kv_free, 1);
+    mbar_init(acc_free, 256);
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t tS = tbase, tV = tbase + 256, tK = tbase + 384;
+
+  if (warp >= 8) {
+    reg_dealloc<kRegsLowKV>();
+    if (warp == 8 || warp >= 10) {
+      // ---------------------------------------------------------- TMA producers
+      // warp 8: K pair + Q ring; warp 10: dZ pair; warp 11: dO
+      const bool leader = elect_one();
+      if (leader) {
+        if (warp == 8) {
+          tma_prefetch(&tm_q);
+          tma_prefetch(&tm_k);
+        } else {
+          tma_prefetch(warp == 10 ? &tm_z : &tm_do);
+        }
+      }
+      int jg = 0, ni = 0;
+      for (int kq = 0;; ++kq) {
+        const int idx = snake_item(kq);
+        if (idx >= n_items) break;
+        const KVItem wi = kv_item(g, idx);
+        if (!wi.valid) continue;
+        const Unit& u = wi.u;
+        LiveQt it{args.first_kb + u.fkb_off, u.nb, u.n_qt, wi.kb0, 0, wi.kb0, 0, 0u, 0u};
+        it.fill(wi.kb0 / 2);
+        int qt = it.next();
+        if (qt >= u.n_qt) continue;  // nothing visited: the warpgroups write zeros
+        if (warp == 8) {
+          if (ni >= 1) mbar_wait(kv_free, (ni - 1) & 1);
+          if (leader) {
+            mbar_expect_tx(bar_kv, C::kPairBytes);
+            for (int w = 0; w < 2; ++w)  // the K tensor map has 64-row boxes
+              for (int c = 0; c < D / 64; ++c)
+                tma_load_4d(&tm_k, bar_kv,
+                            smem + C::kOffK + c * (2 * kBlock * 128) + w * (kBlock * 128), c * 64,
+                            u.trow0 + (wi.kb0 + w) * kBlock, wi.h, u.tb);
+          }
+          __syncwarp();
+        }
+        for (; qt < u.n_qt; qt = it.next(), ++jg) {
+          if (warp == 8) {
+            const int s = jg % ST;
+            if (jg >= ST) mbar_wait(bar_qempty + s, ((jg / ST) - 1) & 1);
+            if (leader) {
+              mbar_expect_tx(bar_qfull + s, C::kQBytes);
+              for (int c = 0; c < D / 64; ++c)
+                tma_load_4d(&tm_q, bar_qfull + s,
+                            smem + C::kOffQ + s * C::kQBytes + c * (kTileM * 128), c * 64,
+                            u.trow0 + qt * kTileM, wi.h, u.tb);
+            }
+          } else if (warp == 10) {
+            if (jg >= 1) mbar_wait(bar_zempty, (jg - 1) & 1);  // dK(jg-1) read dZ
+            if (leader) {
+              mbar_expect_tx(bar_zfull, 2 * kZTileBytes);
+              for (int w = 0; w < 2; ++w)
+                tma_load_3d(&tm_z, bar_zfull, smem + C::kOffZ + w * C::kPBytes, 0, 0,
+                            (int)(u.z_off + ztile(qt, wi.kb0 + w)));
+            }
+          } else {
+            if (jg >= 1) mbar_wait(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
+            if (leader) {
+              mbar_expect_tx(bar_dofull, C::kQBytes);
+              for (int c = 0; c < D / 64; ++c)
+                tma_load_4d(&tm_do, bar_dofull, smem + C::kOffDO + c * (kTileM * 128), c * 64,
+                            u.trow0 + qt * kTileM, wi.h, u.tb);
+            }
+          }
+          __syncwarp();
+        }
+        ++ni;
+      }
+    } else if (warp == 9) {
+      // ---------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);  // Q K^T (N = 2 blocks)
+      constexpr uint32_t idesc_t = idesc_bf16(128, D, 1, 1);    // A^T dO, dZ^T Q: MN-major
+      const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
+      const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ), 16, 1024);
+      const uint64_t dqmn = sdesc_sw128(smem_u32(smem + C::kOffQ), kTileM * 128, 1024);
+      const uint64_t ddomn = sdesc_sw128(smem_u32(smem + C::kOffDO), kTileM * 128, 1024);
+      const uint64_t da = sdesc_sw128(smem_u32(smem + C::kOffA), C::kPBytes, 1024);
+      const uint64_t dz = sdesc_sw128(smem_u32(smem + C::kOffZ), C::kPBytes, 1024);
+      const bool leader = elect_one();
+      auto issue_s = [&](int jg, bool last) {
+        const uint32_t qo = (jg % ST) * C::kQBytes;
+        const int b = jg & 1;
+        mbar_wait(bar_qfull + jg % ST, (jg / ST) & 1);
+        if (jg >= 2) mbar_wait(sempty + b, ((jg >> 1) - 1) & 1);
+        tc_fence_after();
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (2 * kBlock * 128) + (k & 3) * 32;
+            umma_ss_at(tS + b * 128, dq, qo + off, dk, offk, idesc_s, k > 0);
+          }
+          umma_commit(sfull + b);
+          if (last) umma_commit(kv_free);  // the item's K pair may be replaced
+        }
+        __syncwarp();
+      };
+      int jg = 0, ni = 0;
+      for (int kq = 0;; ++kq) {
+        const int idx = snake_item(kq);
+        if (idx >= n_items) break;
+        const KVItem wi = kv_item(g, idx);
+        if (!wi.valid) continue;
+        const Unit& u = wi.u;
+        LiveQt it{args.first_kb + u.fkb_off, u.nb, u.n_qt, wi.kb0, 0, wi.kb0, 0, 0u, 0u};
+        it.fill(wi.kb0 / 2);
+        int n = 0;
+        for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
+        if (n == 0) continue;
+        mbar_wait(bar_kv, ni & 1);
+        issue_s(jg, n == 1);
+        for (int j = 0; j < n; ++j, ++jg) {
+          const int s = jg % ST;
+          // S(j+1) into the other TMEM buffer: it runs while the warpgroups
+          // compute A(j)
+          if (j + 1 < n) issue_s(jg + 1, j + 2 == n);
+          mbar_wait(afull, jg & 1);
+          mbar_wait(bar_dofull, jg & 1);
+          if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
+            for (int k = 0; k < kTileM / 16; ++k)  // dV += A^T dO  (K = query rows)
+              umma_ss_at(tV, da, k * 2048, ddomn, k * 2048, idesc_t, (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(aused);
+            umma_commit(bar_doempty);
+          }
+          __syncwarp();
+          mbar_wait(bar_zfull, jg & 1);
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
+            for (int k = 0; k < kTileM / 16; ++k)  // dK += dZ^T Q
+              umma_ss_at(tK, dz, k * 2048, dqmn, s * C::kQBytes + k * 2048, idesc_t,
+                         (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(bar_zempty);
+            umma_commit(bar_qempty + s);
+            if (j + 1 == n) umma_commit(done);
+          }
+          __syncwarp();
+        }
+        ++ni;
+      }
+    }
+  } else {
+    reg_alloc<kRegsHighKV>();
+    // ------------------------------------------------------------ stick warpgroups
+    // warpgroup w: A of key block kb0 + w for the tile's 128 query rows
+    const int w = warp >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tSw0 = tS + lane_base + w * 64;
+    const uint32_t a_row = smem_u32(smem + C::kOffA + w * C::kPBytes) + r * 128;
+    const float scale = g.scale_log2 * kLn2;
+    int jg = 0, ni = 0;
+    for (int kq = 0;; ++kq) {
+      const int idx = snake_item(kq);
+      if (idx >= n_items) break;
+      const KVItem wi = kv_item(g, idx);
+      if (!wi.valid) continue;
+      const Unit& u = wi.u;
+      const int kb = wi.kb0 + w;
+      LiveQt it{args.first_kb + u.fkb_off, u.nb, u.n_qt, wi.kb0, quarter >> 1, kb, 0, 0u, 0u};
+      it.fill(wi.kb0 / 2);
+      int qt = it.next();
+      const bool any = qt < u.n_qt;
+      const float* Mbase = args.M + u.m_off + (r & 63);
+      auto tix = [&](int qt) -> int64_t {
+        const int qb = min(2 * qt + (r >> 6), u.nb - 1);
+        return tile_index(qb, min(kb, qb)) * kBlock;
+      };
+      auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < u.L; };
+      bool live = is_live(qt);
+      float Ma = Mbase[tix(qt)];
+      for (; qt < u.n_qt; ++jg) {
+        const int my_qb = 2 * qt + (r >> 6);
+        const uint32_t tSw = tSw0 + (jg & 1) * 128;
+        mbar_wait(sfull + (jg & 1), (jg >> 1) & 1);
+        tc_fence_after();
+        const float E = live ? ex2(Ma) : 0.0f;  // dead rows/tiles: A = 0 (M load hidden by the wait)
+        float sv[64];
+        tmem_ld32(tSw, sv);
+        tmem_ld32(tSw + 32, sv + 32);
+        tmem_wait_ld();
+        const bool diag = kb == my_qb;  // warp-uniform
+        // the recompute-mode kernel's A arithmetic exactly (bit-identical results)
+        float sg[64];
+        if (diag) recompute_row<true, false>(sv, sg, g.scale_log2, E, r & 63);
+        else recompute_row<false, false>(sv, sg, g.scale_log2, E, kBlock);
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = pack_bf16(sv[2 * i], sv[2 * i + 1]);
+        tc_fence_before();
+        mbar_arrive(sempty + (jg & 1));  // S(j+2) may overwrite the buffer now
+        const int qt_next = it.next();  // warp-collective
+        const bool live_next = is_live(qt_next);
+        const float Ma_next = Mbase[tix(qt_next)];
+        if (jg >= 1) mbar_wait(aused, (jg - 1) & 1);  // dV of the previous tile read A
+        store_row_sw128(a_row, r, pk);
+        fence_proxy_async_smem();
+        mbar_arrive(afull);
+        qt = qt_next;
+        live = live_next;
+        Ma = Ma_next;
+      }
+
+      // epilogue (as the recompute-mode kernel): lane = key, warp (w, quarter)
+      // owns keys 32*quarter.. and head-dim columns w*D/2..; rows leave through
+      // this warp's slice of the A buffers (free: `done`)
+      if (any) {
+        mbar_wait(done, ni & 1);
+        tc_fence_after();
+      }
+      {
+        constexpr int HD = D / 2;
+        const int key0 = wi.kb0 * kBlock + quarter * 32;
+        const int nvalid = max(0, min(32, u.L - key0));
+        const uint32_t stage = smem_u32(smem + C::kOffA) + (warp & 7) * (32 * HD * 2);
+#pragma unroll 1
+        for (int t = 0; t < 2; ++t) {
+          float a[HD];
+          if (any) {
+            const uint32_t tacc = (t ? tK : tV) + lane_base + w * HD;
+#pragma unroll
+            for (int c = 0; c < HD; c += 32) tmem_ld32(tacc + c, a + c);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int c = 0; c < HD; ++c) a[c] = 0.0f;
+          }
+          if (t == 1 && any) {
+            tc_fence_before();
+            mbar_arrive(acc_free);  // the next item's dV/dK may start
+          }
+          __nv_bfloat16* dst = (t ? args.dk : args.dv) + u.out_off + (int64_t)key0 * g.sl + w * HD;
+          warp_store_rows<HD / 8>(a, t ? scale : 1.0f, stage, dst, g.sl, nvalid);
+        }
+      }
+      if (any) ++ni;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) tmem_dealloc<C::kTmemCols>(tbase);
+}
+
 template <int D>
 static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                      const CUtensorMap& tv, const BwdArgs& a, int phases, cudaStream_t stream) {
+                      const CUtensorMap& tv, const CUtensorMap& tz, const BwdArgs& a, int phases,
+                      bool store, cudaStream_t stream) {
   const unsigned BH = (unsigned)(a.g.B * a.g.H);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (phases & 1) {
     using C = BwdQCfg<D>;
-    auto kern = sb_bwd_q_kernel<D>;
+    auto kern = store ? sb_bwd_q_kernel<D, true> : sb_bwd_q_kernel<D, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return (int)e;
     if ((e = cudaMemsetAsync(a.sched, 0, sizeof(unsigned), stream)) != cudaSuccess) return (int)e;
     // persistent: one CTA per SM (fewer if there are fewer work items)
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned items = (unsigned)((a.g.n_qt + 1) / 2) * BH;
     kern<<<items < (unsigned)sms ? items : (unsigned)sms, kBwdThreads, C::kSmem, stream>>>(
-        tq, tdo, tk, tv, a);
+        tq, tdo, tk, tv, tz, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   }
   if (phases & 2) {
-    using C = BwdKVCfg<D>;
-    auto kern = sb_bwd_kv_kernel<D>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return (int)e;
-    if ((e = cudaMemsetAsync(a.sched + 1, 0, sizeof(unsigned), stream)) != cudaSuccess)
-      return (int)e;
-    // persistent: one CTA per SM (fewer if there are fewer work items)
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned items = (unsigned)((a.g.nb + 1) / 2) * BH;
-    kern<<<items < (unsigned)sms ? items : (unsigned)sms, kBwdThreads, C::kSmem, stream>>>(
-        tq, tdo, tk, tv, a);
+    const unsigned grid = items < (unsigned)sms ? items : (unsigned)sms;
+    cudaError_t e;
+    if (store) {
+      using C = BwdKVSCfg<D>;
+      auto kern = sb_bwd_kvs_kernel<D>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+      if (e != cudaSuccess) return (int)e;
+      kern<<<grid, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tz, a);
+    } else {
+      using C = BwdKVCfg<D>;
+      auto kern = sb_bwd_kv_kernel<D>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+      if (e != cudaSuccess) return (int)e;
+      if ((e = cudaMemsetAsync(a.sched + 1, 0, sizeof(unsigned), stream)) != cudaSuccess)
+        return (int)e;
+      kern<<<grid, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tv, a);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   }
   return 0;
 }
 
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                 const CUtensorMap& tv, const BwdArgs& a, int phases, cudaStream_t stream) {
-  if (D == 128) return launch_bwd<128>(tq, tdo, tk, tv, a, phases, stream);
-  if (D == 64) return launch_bwd<64>(tq, tdo, tk, tv, a, phases, stream);
+                 const CUtensorMap& tv, const CUtensorMap& tz, const BwdArgs& a, int phases,
+                 bool store, cudaStream_t stream) {
+  if (D == 128) return launch_bwd<128>(tq, tdo, tk, tv, tz, a, phases, store, stream);
+  if (D == 64) return launch_bwd<64>(tq, tdo, tk, tv, tz, a, phases, store, stream);
   return -1;
 }
 

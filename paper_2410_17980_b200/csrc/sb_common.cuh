@@ -44,7 +44,15 @@ struct Unit {
   int64_t m_off, fkb_off;      // element offsets into M / N and first_kb
   int64_t rem_off, rem_stride; // log_rem / row_offset element of row r: rem_off + r*rem_stride
   int64_t out_off;             // element offset of row 0 in q/k/v/o/do/dq/dk/dv
+  int64_t z_off;               // first dZ tile of the unit in the tile workspace (ztile)
 };
+
+// dZ tile workspace (store mode of the backward): phase 1 writes every 128-row x
+// 64-key dZ tile it computes, phase 2 reads them instead of recomputing dZ.  Per
+// unit, tile (qt, kb) for kb < 2*qt + 2 sits at z_off + ztile(qt, kb); 16 KB each
+// (the 128B-swizzled smem image, as the MMA reads it).
+__device__ __forceinline__ int64_t ztile(int qt, int kb) { return (int64_t)qt * (qt + 1) + kb; }
+constexpr int kZTileBytes = kTileM * kBlock * 2;
 
 __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
   Unit u;
@@ -61,12 +69,15 @@ __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
     u.rem_off = unit * g.L;
     u.rem_stride = 1;
     u.out_off = (int64_t)b * g.sb + (int64_t)h * g.sh;
+    u.z_off = unit * g.n_qt * (g.n_qt + 1);
   } else {
-    int64_t tiles_before = 0, nb_before = 0;
+    int64_t tiles_before = 0, nb_before = 0, z_before = 0;
     for (int i = 0; i < b; ++i) {
-      const int nbi = (g.cu[i + 1] - g.cu[i] + kBlock - 1) / kBlock;
+      const int Li = g.cu[i + 1] - g.cu[i];
+      const int nbi = (Li + kBlock - 1) / kBlock, nqi = (Li + kTileM - 1) / kTileM;
       tiles_before += (int64_t)nbi * (nbi + 1) / 2;
       nb_before += nbi;
+      z_before += (int64_t)nqi * (nqi + 1);
     }
     const int s0 = g.cu[b];
     u.L = g.cu[b + 1] - s0;
@@ -80,6 +91,7 @@ __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
     u.rem_off = (int64_t)s0 * g.H + h;
     u.rem_stride = g.H;
     u.out_off = (int64_t)s0 * g.sl + (int64_t)h * g.sh;
+    u.z_off = z_before * g.H + (int64_t)h * u.n_qt * (u.n_qt + 1);
   }
   return u;
 }

@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -37,6 +38,10 @@ from . import _lib
 
 DEFAULT_BLOCK = 64
 SCHED_HEADER = 64  # floats at the start of M / N holding the kernels' work-queue counters
+# Store mode of the backward (phase 1 writes its dZ tiles, phase 2 reads them instead of
+# recomputing dO.V^T and dZ; bit-identical results) is used when its workspace is at most
+# this many bytes (C2: 2.1 GiB; C3 at L=32768 would need 33 GiB and recomputes instead).
+TILE_WORKSPACE_MAX_BYTES = int(float(os.environ.get("SB_TILE_WORKSPACE_MAX_GB", "8")) * 2**30)
 SKIP_EPS_BF16 = 1e-6  # the reference's f32 default (blocked.py:43) is used for bf16
 
 
@@ -102,6 +107,7 @@ class BlockedCache:
     skip_eps: float
     cu_seqlens: torch.Tensor | None = None  # varlen: device int32 [n_seq+1]
     max_seqlen: int = 0
+    cu_host: torch.Tensor | None = None     # varlen: host copy of cu_seqlens
 
 
 def _ptr(t):
@@ -208,7 +214,7 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
     visited = int(cnt[0].item()) if counters else -1
     stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
     cache = BlockedCache(q, k, v, scale, None, log_rem, first_kb, M, skip, skip_eps,
-                         cu_seqlens=cu, max_seqlen=max_L)
+                         cu_seqlens=cu, max_seqlen=max_L, cu_host=host_c)
     return o, log_rem, stats, cache
 
 
@@ -265,12 +271,27 @@ def sb_forward_blocked(q, k, v, layout=None, **kw):
     return o, cache
 
 
+def tile_workspace_bytes(cache: BlockedCache) -> int:
+    """Bytes of the dZ tile workspace the store-mode backward needs for this cache."""
+    lib = _lib.load()
+    p = _params(cache.q, cache.scale, cache.skip, cache.skip_eps, cu_seqlens=cache.cu_seqlens,
+                max_seqlen=cache.max_seqlen)
+    host = None if cache.cu_host is None else ctypes.c_void_p(cache.cu_host.data_ptr())
+    return int(lib.sb_bwd_tile_bytes(ctypes.byref(p), host))
+
+
 def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | None = None,
-                              row_offset=None, *, out=None, phases: int = 3):
+                              row_offset=None, *, out=None, phases: int = 3,
+                              store_tiles: bool | None = None, tiles=None):
     """blocked_backward_twophase (blocked.py:299-392) over every (b, h) unit.
 
     Returns (d_q, d_k, d_v, n_stored_tiles).  row_offset (B, H, L) float32 is
     subtracted from dO.V^T per query row (blocked.py:241-242).
+
+    store_tiles: None = store mode when its workspace fits TILE_WORKSPACE_MAX_BYTES,
+    True/False to force.  `tiles` passes a preallocated workspace (uint8 CUDA tensor of
+    tile_workspace_bytes(cache)); callers running the phases one by one must pass the
+    same one to both.
     """
     if layout is not None and layout != cache.layout:
         raise ValueError("layout does not match the one the cache was built with")  # :398-399
@@ -299,9 +320,16 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
                              "(total_tokens, heads) for varlen")
     if cache.cu_seqlens is not None and cache.max_seqlen == 0:
         return dq.zero_(), dk.zero_(), dv.zero_(), 0
-    _lib.check(lib.sb_bwd_phase(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
-                                _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M),
-                                _ptr(N), _ptr(dq), _ptr(dk), _ptr(dv), int(phases), _stream()))
+    if tiles is None:
+        nbytes = tile_workspace_bytes(cache)
+        use = (nbytes <= TILE_WORKSPACE_MAX_BYTES) if store_tiles is None else bool(store_tiles)
+        if use and nbytes > 0:
+            tiles = torch.empty(nbytes, device=q.device, dtype=torch.uint8)
+    nbytes = 0 if tiles is None else tiles.numel()
+    _lib.check(lib.sb_bwd_ws(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
+                             _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M), _ptr(N),
+                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(tiles), nbytes, int(phases),
+                             _stream()))
     n_stored = ((cache.M.numel() - SCHED_HEADER) // DEFAULT_BLOCK if cache.cu_seqlens is not None
                 else cache.layout.n_tiles * q.shape[0] * q.shape[1])
     return dq, dk, dv, n_stored
@@ -323,7 +351,7 @@ class _StickBreakingFn(torch.autograd.Function):
         q, k, v, log_rem, first_kb, M = ctx.saved_tensors
         c = ctx.cache
         cache = BlockedCache(q, k, v, c.scale, c.layout, log_rem, first_kb, M, c.skip, c.skip_eps,
-                             cu_seqlens=c.cu_seqlens, max_seqlen=c.max_seqlen)
+                             cu_seqlens=c.cu_seqlens, max_seqlen=c.max_seqlen, cu_host=c.cu_host)
         if d_o is None:
             d_o = torch.zeros_like(q)
         # rem_j = 1 - sum_i A_ij  =>  dL/dA_ij -= dL/drem_j : the reference's

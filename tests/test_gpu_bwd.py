@@ -23,19 +23,38 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def _run(q, k, v, d_o, skip=False, row_offset=None):
+def _run(q, k, v, d_o, skip=False, row_offset=None, store=None):
     import paper_2410_17980_b200 as sb
     o, log_rem, stats, cache = sb.blocked_forward(q, k, v, skip=skip, skip_eps=1e-6)
-    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, row_offset=row_offset)
+    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, row_offset=row_offset,
+                                                 store_tiles=store)
     torch.cuda.synchronize()
     return o, log_rem, stats, dq, dk, dv
 
 
+@pytest.mark.parametrize("B,H,L,d,skip,family,ro", [
+    (1, 2, 320, 128, False, "random", False), (2, 1, 200, 64, False, "random", True),
+    (1, 1, 1000, 128, False, "random", False), (1, 2, 130, 128, False, "random", True),
+    (1, 2, 1024, 128, True, "shift", False), (1, 2, 512, 128, True, "saturating", False),
+    (1, 2, 1, 64, False, "random", False), (1, 3, 900, 64, True, "random", True)])
+def test_store_mode_bit_identical(B, H, L, d, skip, family, ro):
+    """Store mode (phase 2 reads phase 1's dZ tiles) gives the recompute mode's
+    gradients bit for bit: the stored tiles are exactly what phase 2 recomputes."""
+    q, k, v, d_o = make_qkv(B, H, L, d, seed=L + d, family=family)
+    row_offset = (torch.randn(B, H, L, generator=torch.Generator().manual_seed(3)).cuda()
+                  if ro else None)
+    a = _run(q, k, v, d_o, skip=skip, row_offset=row_offset, store=False)
+    b = _run(q, k, v, d_o, skip=skip, row_offset=row_offset, store=True)
+    for x, y, n in zip(a[3:], b[3:], ("dq", "dk", "dv")):
+        assert torch.equal(x, y), n
+
+
+@pytest.mark.parametrize("store", [False, True])
 @pytest.mark.parametrize("B,H,L,d", [(1, 2, 256, 64), (1, 2, 320, 128), (1, 1, 64, 128),
                                      (2, 1, 200, 64), (1, 1, 1000, 128), (1, 1, 130, 128)])
-def test_backward_matches_oracle(B, H, L, d):
+def test_backward_matches_oracle(B, H, L, d, store):
     q, k, v, d_o = make_qkv(B, H, L, d, seed=L + 3 * d)
-    o, _, _, dq, dk, dv = _run(q, k, v, d_o)
+    o, _, _, dq, dk, dv = _run(q, k, v, d_o, store=store)
     ref = oracle_fwd(q, k, v)
     rdq, rdk, rdv, _ = oracle_bwd(q, k, v, d_o, ref)
     errs = [rel_to_max(to64(a), b) for a, b in ((dq, rdq), (dk, rdk), (dv, rdv))]

@@ -41,14 +41,15 @@ def seq(t, cu, b):
     return t[s0:s1].transpose(0, 1).unsqueeze(0).contiguous()
 
 
+@pytest.mark.parametrize("store", [False, True])
 @pytest.mark.parametrize("d", [64, 128])
-def test_varlen_equals_per_sequence_runs(d):
+def test_varlen_equals_per_sequence_runs(d, store):
     import paper_2410_17980_b200 as sb
     lens = [100, 0, 257, 64, 1, 513, 130]
     H = 2
     (q, k, v, d_o), cu = packed(lens, H, d, seed=d)
     o, log_rem, st, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu)
-    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o)
+    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, store_tiles=store)
     torch.cuda.synchronize()
     assert st.visited == st.total == H * sum((n + 63) // 64 * ((n + 63) // 64 + 1) // 2
                                              for n in lens)
@@ -57,7 +58,7 @@ def test_varlen_equals_per_sequence_runs(d):
             continue
         qs, ks, vs, ds = (seq(t, cu, b) for t in (q, k, v, d_o))
         o1, lr1, _, c1 = sb.blocked_forward(qs, ks, vs)
-        dq1, dk1, dv1, _ = sb.blocked_backward_twophase(c1, ds)
+        dq1, dk1, dv1, _ = sb.blocked_backward_twophase(c1, ds, store_tiles=False)
         s0, s1 = int(cu[b]), int(cu[b + 1])
         assert torch.equal(seq(o, cu, b), o1), b
         assert torch.equal(log_rem[s0:s1].transpose(0, 1).unsqueeze(0), lr1), b

@@ -27,9 +27,10 @@ def main(path):
         ev[1].record()
         out = (torch.empty_like(cache.M), torch.empty_like(q), torch.empty_like(q),
                torch.empty_like(q))
-        ops.blocked_backward_twophase(cache, do, phases=1, out=out)
+        tiles = torch.empty(ops.tile_workspace_bytes(cache), device=dev, dtype=torch.uint8)
+        ops.blocked_backward_twophase(cache, do, phases=1, out=out, tiles=tiles)
         ev[2].record()
-        ops.blocked_backward_twophase(cache, do, phases=2, out=out)
+        ops.blocked_backward_twophase(cache, do, phases=2, out=out, tiles=tiles)
         ev[3].record()
     torch.cuda.synchronize()
     print(path, "fwd %.3f p1 %.3f p2 %.3f ms" % (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]),
