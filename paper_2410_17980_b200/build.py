@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False,
     if variant:
         lib = os.path.join(HERE, f"libsbattn_{variant}.so")
         tag = "_" + variant
-        extra = {"nomath": ["-DSB_NOMATH"], "trace_nomath": ["-DSB_NOMATH", "-DSB_TRACE"]}[variant]
+        extra = {"nomath": ["-DSB_NOMATH"], "trace_nomath": ["-DSB_NOMATH", "-DSB_TRACE"],
+                 "noz": ["-DSB_NOZ"], "nomath_noz": ["-DSB_NOMATH", "-DSB_NOZ"]}[variant]
     if not force and not _stale(lib):
         return lib
     jobs = []

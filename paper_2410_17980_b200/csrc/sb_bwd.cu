@@ -1047,17 +1047,111 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 8) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
+// A only (store-mode phase 2), software-pipelined across the four 16-column
+// groups, right to left: group g's ex2 pass (MUFU) is interleaved with group
+// g+1's product pass (FMA pipe), so one warp keeps both pipes busy instead of
+// running 64 ex2 back to back and then 128 multiplies.  Per element the
+// arithmetic is exactly recompute_row<kDiag, false>'s fast path (same
+// operations, same order: bit-identical A).  On exit pk[] holds A as bf16x2
+// and s[] the masked t values; returns false if a group product reached 2^64
+// (the caller redoes that row with the per-element path).
+template <bool kDiag>
+__device__ __forceinline__ bool recompute_a_pipe(float* s, uint32_t* pk, float scale_log2, float E,
+                                                 int lim) {
+#ifdef SB_NOMATH  // tuning ablation: pipeline without the stick math
+#pragma unroll
+  for (int c = 0; c < kBlock; c += 2) pk[c >> 1] = pack_bf16(s[c] * E, s[c + 1] * E);
+  return true;
+#endif
+  float P[64];
+  float tot = 1.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {  // prologue: pass 1 of group 3
+    const int c = 48 + i;
+    float tt = ex2(s[c] * scale_log2);
+    if (kDiag) tt = c < lim ? tt : 0.0f;
+    s[c] = tt;
+    tot = fmaf(tot, tt, tot);
+    P[c] = tot;
+  }
+  bool ok = tot < kBatchedMax;
+  float Kn = E * rcp(tot);  // K of the group whose product pass runs next
+  float Q = Kn;
+#pragma unroll
+  for (int g = 2; g >= 0; --g) {
+    tot = 1.0f;
+    float a0 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = 16 * g + i;  // pass 1, group g
+      float tt = ex2(s[c] * scale_log2);
+      if (kDiag) tt = c < lim ? tt : 0.0f;
+      s[c] = tt;
+      tot = fmaf(tot, tt, tot);
+      P[c] = tot;
+      const int c2 = c + 16;  // pass 2, group g + 1
+      const float u = i ? s[c2] * P[c2 - 1] : s[c2];
+      const float a = u * Kn;
+      if (i & 1) pk[c2 >> 1] = pack_bf16(a0, a);
+      else a0 = a;
+    }
+    ok = ok && (tot < kBatchedMax);
+    Kn = Q * rcp(tot);
+    Q = Kn;
+  }
+  float a0 = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {  // epilogue: pass 2 of group 0
+    const float u = i ? s[i] * P[i - 1] : s[i];
+    const float a = u * Kn;
+    if (i & 1) pk[i >> 1] = pack_bf16(a0, a);
+    else a0 = a;
+  }
+  return ok;
+}
+
 // ============================================================================
 // Phase 2, store mode: dZ tiles come from the workspace phase 1 wrote, so a
 // key pair's tile needs only S = Q [K0;K1]^T and A (no dO V^T, no dZ math):
 //   dV += [A0 A1]^T dO, dK += [dZ0 dZ1]^T Q  (dZ TMA-loaded).
-// Tensor-pipe order per tile j: S(j+1) (double-buffered in TMEM, runs while the
-// warpgroups compute A(j)), dV(j), dK(j).  Q has 3 stages (S(j+1) and dK(j)
-// hold two; the third is in flight), dO and dZ one each; three producer warps
-// (K+Q, dZ, dO) refill each buffer the moment the MMA reading it completes.
+// Tensor-pipe order per tile j: dK(j) (needs only loaded data), S(j+1)
+// (double-buffered in TMEM, runs while the warpgroups compute A(j)), dV(j).
+// Issuing dK first frees Q(j) and dZ(j) early, so Q and dZ rings of 2 stages
+// have a whole tile of slack for their refills; dO (single) is refilled while
+// dK(j+1) and S(j+2) run.  Three producer warps (K+Q, dZ, dO) refill each
+// buffer the moment the MMA reading it completes, prefetching into L2 ahead.
+// Producer look-ahead: walks the CTA's (item, query tile) sequence kPrefetch
+// tiles ahead of the loads and prefetches those tiles into L2, so a buffer's
+// refill (issued when the MMA reading it completes) hits L2 instead of HBM.
+constexpr int kPrefetch = 4;
+struct KVCursor {
+  const Geom* g;
+  const int* first_kb;
+  int n_items, kq, qt;
+  KVItem wi;
+  LiveQt it;
+  __device__ __forceinline__ bool open_next_item() {
+    for (;;) {
+      const int idx = snake_item(++kq);
+      if (idx >= n_items) return false;
+      wi = kv_item(*g, idx);
+      if (!wi.valid) continue;
+      it = LiveQt{first_kb + wi.u.fkb_off, wi.u.nb, wi.u.n_qt, wi.kb0, 0, wi.kb0, 0, 0u, 0u};
+      it.fill(wi.kb0 / 2);
+      qt = it.next();
+      if (qt < wi.u.n_qt) return true;
+    }
+  }
+  // next tile; false at the end of the CTA's work (warp-collective)
+  __device__ __forceinline__ bool advance() {
+    qt = it.next();
+    return qt < wi.u.n_qt || open_next_item();
+  }
+};
+
 template <int D>
 struct BwdKVSCfg {
-  static constexpr int kStages = 3;                       // Q ring
+  static constexpr int kStages = 2;                       // Q ring
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kPairBytes = 2 * kBlock * D * 2;  // K of both key blocks
   static constexpr int kPBytes = kTileM * kBlock * 2;    // A / dZ of one key block
@@ -1065,9 +1159,9 @@ struct BwdKVSCfg {
   static constexpr int kOffQ = kOffK + kPairBytes;
   static constexpr int kOffDO = kOffQ + kStages * kQBytes;  // single buffer (free after dV)
   static constexpr int kOffA = kOffDO + kQBytes;            // key block 0 then 1
-  static constexpr int kOffZ = kOffA + 2 * kPBytes;         // dZ of key block 0 then 1
-  static constexpr int kOffBar = kOffZ + 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 9;
+  static constexpr int kOffZ = kOffA + 2 * kPBytes;         // dZ ring: 2 x (block 0, block 1)
+  static constexpr int kOffBar = kOffZ + 2 * 2 * kPBytes;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 4 + 9;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
@@ -1094,9 +1188,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_qempty = bar_qfull + ST;
   uint64_t* bar_dofull = bar_qempty + ST;
   uint64_t* bar_doempty = bar_dofull + 1;
-  uint64_t* bar_zfull = bar_doempty + 1;  // dZ pair landed
-  uint64_t* bar_zempty = bar_zfull + 1;   // dK read it
-  uint64_t* sfull = bar_zempty + 1;  // [2] S double-buffered in TMEM (cols 0 / 128)
+  uint64_t* bar_zfull = bar_doempty + 1;  // [2] dZ pair landed
+  uint64_t* bar_zempty = bar_zfull + 2;   // [2] dK read it
+  uint64_t* sfull = bar_zempty + 2;  // [2] S double-buffered in TMEM (cols 0 / 128)
   uint64_t* sempty = sfull + 2;      // [2]
   uint64_t* afull = sfull + 4;
   uint64_t* aused = sfull + 5;
@@ -1113,8 +1207,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(bar_dofull, 1);
     mbar_init(bar_doempty, 1);
-    mbar_init(bar_zfull, 1);
-    mbar_init(bar_zempty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar_zfull + s, 1);
+      mbar_init(bar_zempty + s, 1);
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(sfull + s, 1);
       mbar_init(sempty + s, 256);
@@ -1147,6 +1243,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_prefetch(warp == 10 ? &tm_z : &tm_do);
         }
       }
+      // L2 look-ahead (see KVCursor): this warp's stream only
+      KVCursor ahead{&g, args.first_kb, n_items, -1, 0};
+      bool more = ahead.open_next_item();
+      auto prefetch_one = [&]() {
+        if (!more) return;
+        if (leader) {
+          const Unit& v = ahead.wi.u;
+          if (warp == 10) {
+            for (int w = 0; w < 2; ++w)
+              tma_prefetch_3d(&tm_z, 0, 0, (int)(v.z_off + ztile(ahead.qt, ahead.wi.kb0 + w)));
+          } else {
+            for (int c = 0; c < D / 64; ++c)
+              tma_prefetch_4d(warp == 8 ? &tm_q : &tm_do, c * 64, v.trow0 + ahead.qt * kTileM,
+                              ahead.wi.h, v.tb);
+          }
+        }
+        __syncwarp();
+        more = ahead.advance();
+      };
+      for (int i = 0; i < kPrefetch; ++i) prefetch_one();
       int jg = 0, ni = 0;
       for (int kq = 0;; ++kq) {
         const int idx = snake_item(kq);
@@ -1171,9 +1287,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
         }
         for (; qt < u.n_qt; qt = it.next(), ++jg) {
+          prefetch_one();
           if (warp == 8) {
             const int s = jg % ST;
             if (jg >= ST) mbar_wait(bar_qempty + s, ((jg / ST) - 1) & 1);
+            SB_TR(args, 3, jg, 0);
             if (leader) {
               mbar_expect_tx(bar_qfull + s, C::kQBytes);
               for (int c = 0; c < D / 64; ++c)
@@ -1182,15 +1300,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                             u.trow0 + qt * kTileM, wi.h, u.tb);
             }
           } else if (warp == 10) {
-            if (jg >= 1) mbar_wait(bar_zempty, (jg - 1) & 1);  // dK(jg-1) read dZ
+            const int z = jg & 1;
+            if (jg >= 2) mbar_wait(bar_zempty + z, ((jg >> 1) - 1) & 1);  // dK(jg-2) read dZ
+            SB_TR(args, 3, jg, 2);
             if (leader) {
-              mbar_expect_tx(bar_zfull, 2 * kZTileBytes);
+#ifdef SB_NOZ  // tuning ablation: no dZ traffic (dK reads whatever is in the buffer)
+              mbar_arrive(bar_zfull + z);
+#else
+              mbar_expect_tx(bar_zfull + z, 2 * kZTileBytes);
               for (int w = 0; w < 2; ++w)
-                tma_load_3d(&tm_z, bar_zfull, smem + C::kOffZ + w * C::kPBytes, 0, 0,
+                tma_load_3d(&tm_z, bar_zfull + z, smem + C::kOffZ + (2 * z + w) * C::kPBytes, 0, 0,
                             (int)(u.z_off + ztile(qt, wi.kb0 + w)));
+#endif
             }
           } else {
             if (jg >= 1) mbar_wait(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
+            SB_TR(args, 3, jg, 4);
             if (leader) {
               mbar_expect_tx(bar_dofull, C::kQBytes);
               for (int c = 0; c < D / 64; ++c)
@@ -1216,8 +1341,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       auto issue_s = [&](int jg, bool last) {
         const uint32_t qo = (jg % ST) * C::kQBytes;
         const int b = jg & 1;
+        SB_TR(args, 2, jg, 0);
         mbar_wait(bar_qfull + jg % ST, (jg / ST) & 1);
+        SB_TR(args, 2, jg, 1);
         if (jg >= 2) mbar_wait(sempty + b, ((jg >> 1) - 1) & 1);
+        SB_TR(args, 2, jg, 2);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -1246,13 +1374,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(bar_kv, ni & 1);
         issue_s(jg, n == 1);
         for (int j = 0; j < n; ++j, ++jg) {
-          const int s = jg % ST;
+          const int s = jg % ST, z = jg & 1;
+          mbar_wait(bar_zfull + z, (jg >> 1) & 1);
+          SB_TR(args, 2, jg, 7);
+          if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);  // epilogue read dK/dV
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
+            for (int k = 0; k < kTileM / 16; ++k)  // dK += dZ^T Q
+              umma_ss_at(tK, dz, 2 * z * C::kPBytes + k * 2048, dqmn, s * C::kQBytes + k * 2048,
+                         idesc_t, (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(bar_zempty + z);
+            umma_commit(bar_qempty + s);  // S(j) and dK(j) read Q(j)
+          }
+          __syncwarp();
           // S(j+1) into the other TMEM buffer: it runs while the warpgroups
           // compute A(j)
           if (j + 1 < n) issue_s(jg + 1, j + 2 == n);
           mbar_wait(afull, jg & 1);
+          SB_TR(args, 2, jg, 4);
           mbar_wait(bar_dofull, jg & 1);
-          if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);
+          SB_TR(args, 2, jg, 5);
           tc_fence_after();
           if (leader) {
 #pragma unroll
@@ -1260,17 +1402,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               umma_ss_at(tV, da, k * 2048, ddomn, k * 2048, idesc_t, (j > 0 || k > 0) ? 1u : 0u);
             umma_commit(aused);
             umma_commit(bar_doempty);
-          }
-          __syncwarp();
-          mbar_wait(bar_zfull, jg & 1);
-          tc_fence_after();
-          if (leader) {
-#pragma unroll
-            for (int k = 0; k < kTileM / 16; ++k)  // dK += dZ^T Q
-              umma_ss_at(tK, dz, k * 2048, dqmn, s * C::kQBytes + k * 2048, idesc_t,
-                         (j > 0 || k > 0) ? 1u : 0u);
-            umma_commit(bar_zempty);
-            umma_commit(bar_qempty + s);
             if (j + 1 == n) umma_commit(done);
           }
           __syncwarp();
@@ -1289,6 +1420,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t tSw0 = tS + lane_base + w * 64;
     const uint32_t a_row = smem_u32(smem + C::kOffA + w * C::kPBytes) + r * 128;
     const float scale = g.scale_log2 * kLn2;
+    const bool tr = quarter == 0 && lane == 0;
+    if (tr) SB_TR(args, w, 0, 14);
     int jg = 0, ni = 0;
     for (int kq = 0;; ++kq) {
       const int idx = snake_item(kq);
@@ -1308,11 +1441,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       auto is_live = [&](int qt) -> bool { return it.mine_live(qt) && qt * kTileM + r < u.L; };
       bool live = is_live(qt);
+      // M snapshots are loaded two tiles ahead (a global load's latency under
+      // this kernel's traffic exceeds one tile)
       float Ma = Mbase[tix(qt)];
+      float Ma1;
+      {
+        LiveQt peek = it;
+        Ma1 = Mbase[tix(peek.next())];
+      }
       for (; qt < u.n_qt; ++jg) {
         const int my_qb = 2 * qt + (r >> 6);
         const uint32_t tSw = tSw0 + (jg & 1) * 128;
+        if (tr) SB_TR(args, w, jg, 0);
         mbar_wait(sfull + (jg & 1), (jg >> 1) & 1);
+        if (tr) SB_TR(args, w, jg, 1);
         tc_fence_after();
         const float E = live ? ex2(Ma) : 0.0f;  // dead rows/tiles: A = 0 (M load hidden by the wait)
         float sv[64];
@@ -1321,21 +1463,47 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_wait_ld();
         const bool diag = kb == my_qb;  // warp-uniform
         // the recompute-mode kernel's A arithmetic exactly (bit-identical results)
-        float sg[64];
-        if (diag) recompute_row<true, false>(sv, sg, g.scale_log2, E, r & 63);
-        else recompute_row<false, false>(sv, sg, g.scale_log2, E, kBlock);
         uint32_t pk[32];
+        const bool ok = diag ? recompute_a_pipe<true>(sv, pk, g.scale_log2, E, r & 63)
+                             : recompute_a_pipe<false>(sv, pk, g.scale_log2, E, kBlock);
+        if (__any_sync(0xffffffffu, !ok)) {
+          // a group product of (1+t) reached 2^64: recompute_row's per-element
+          // path for those rows (t recomputed from S, identically)
+          tmem_ld32(tSw, sv);
+          tmem_ld32(tSw + 32, sv + 32);
+          tmem_wait_ld();
+          if (!ok) {
+            const int lim = diag ? (r & 63) : kBlock;
+            float Ql = E, an = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = pack_bf16(sv[2 * i], sv[2 * i + 1]);
+            for (int c = kBlock - 1; c >= 0; --c) {
+              float t = ex2(sv[c] * g.scale_log2);
+              if (c >= lim) t = 0.0f;
+              const float rr = rcp(1.0f + t);
+              const float sgm = fminf(t * rr, 1.0f);
+              const float a = sgm * Ql;
+              Ql *= rr;
+              if (c & 1) an = a;
+              else pk[c >> 1] = pack_bf16(a, an);
+            }
+          }
+        }
         tc_fence_before();
+        if (tr) SB_TR(args, w, jg, 2);
         mbar_arrive(sempty + (jg & 1));  // S(j+2) may overwrite the buffer now
         const int qt_next = it.next();  // warp-collective
         const bool live_next = is_live(qt_next);
-        const float Ma_next = Mbase[tix(qt_next)];
+        const float Ma_next = Ma1;
+        {
+          LiveQt peek = it;
+          Ma1 = Mbase[tix(peek.next())];
+        }
         if (jg >= 1) mbar_wait(aused, (jg - 1) & 1);  // dV of the previous tile read A
+        if (tr) SB_TR(args, w, jg, 3);
         store_row_sw128(a_row, r, pk);
         fence_proxy_async_smem();
         mbar_arrive(afull);
+        if (tr) SB_TR(args, w, jg, 4);
         qt = qt_next;
         live = live_next;
         Ma = Ma_next;
@@ -1346,6 +1514,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // this warp's slice of the A buffers (free: `done`)
       if (any) {
         mbar_wait(done, ni & 1);
+        if (tr && ni == 0) SB_TR(args, w, 0, 15);
         tc_fence_after();
       }
       {
