@@ -262,11 +262,15 @@ def main():
 
     G = gemm_flops(B, H, L, D)
     alg_flops = 7 * G  # fwd 2G + bwd 5G (FA convention)
-    exec_flops = 9 * G  # fwd 2G + phase 1 3G + phase 2 4G (recompute of QK^T, dO V^T)
+    # executed: fwd 2G (QK^T, AV) + phase 1 3G (QK^T, dO V^T, dZ K) + phase 2: store mode
+    # 3G (QK^T, A^T dO, dZ^T Q; dZ read from phase 1's tiles), recompute mode 4G
+    store = step.tiles is not None
+    p2_exec = 3 * G if store else 4 * G
+    exec_flops = 5 * G + p2_exec
     tflops = world * alg_flops * K / (total_ms / 1e3) / 1e12
     burst, sustained, peak_kind = load_peaks()
-    kernels = {"sb_fwd_kernel": (fwd_ms, 2 * G, 2 * G), "sb_bwd_q_kernel": (p1_ms, 3 * G, 3 * G),
-               "sb_bwd_kv_kernel": (p2_ms, 2 * G, 4 * G)}
+    kernels = {"sb_fwd_pp_kernel": (fwd_ms, 2 * G, 2 * G), "sb_bwd_q_kernel": (p1_ms, 3 * G, 3 * G),
+               ("sb_bwd_kvs_kernel" if store else "sb_bwd_kv_kernel"): (p2_ms, 2 * G, p2_exec)}
     dom = max(kernels, key=lambda n: kernels[n][0])
     d_ms, d_alg, d_exec = kernels[dom]
     achieved = d_alg / (d_ms / 1e3) / 1e12
@@ -393,7 +397,9 @@ def main():
         "config": {"workload": WORKLOAD, "batch_per_gpu": B, "heads": H, "seq_len": L,
                    "head_dim": D, "global_batch": B * world,
                    "parallelism": f"(b,h) units sharded, {world} independent ranks, no collective",
-                   "l2": "inputs (4 x 128 MiB bf16 per rank) exceed the 126 MB L2; no flush"},
+                   "l2": "inputs (4 x 128 MiB bf16 per rank) exceed the 126 MB L2; no flush",
+                   "backward": ("store mode (phase 1 writes dZ tiles, %.2f GB workspace)"
+                                % (step.tiles.numel() / 1e9) if store else "recompute mode")},
         "tflops": tflops, "tflops_note": "algorithmic 7*B*H*L^2*d per step (FA causal convention)",
         "executed_tflops": world * exec_flops * K / (total_ms / 1e3) / 1e12,
         "ms": {"fwd": fwd_ms, "bwd_phase1": p1_ms, "bwd_phase2": p2_ms},

@@ -139,7 +139,9 @@ def lpt_assign_units(lengths, heads: int, world: int, tol: float = 1.02):
 def shard_varlen_units(x: torch.Tensor, cu_host: torch.Tensor, units, G: int):
     """Pack this rank's (sequence, head-group) units into ONE packed batch with
     H/G heads: unit (i, g) becomes a "sequence" holding tokens of sequence i and
-    heads g*H/G .. (g+1)*H/G-1.  Returns (x_local (T_r, H/G, d), cu_local)."""
+    heads g*H/G .. (g+1)*H/G-1.  Returns (x_local (T_r, H/G, d), cu_local) with
+    cu_local on the HOST: pass it straight to blocked_forward /
+    stickbreaking_attention, which then plan without a device sync."""
     hg = x.shape[1] // G
     parts = [x[int(cu_host[i]): int(cu_host[i + 1]), g * hg:(g + 1) * hg] for i, g in units]
     lens = [p.shape[0] for p in parts]
@@ -147,4 +149,4 @@ def shard_varlen_units(x: torch.Tensor, cu_host: torch.Tensor, units, G: int):
     if lens:
         cu[1:] = torch.cumsum(torch.tensor(lens, dtype=torch.int64), 0).to(torch.int32)
     local = torch.cat(parts, 0) if parts else x[:0, :hg]
-    return local.contiguous(), cu.to(x.device)
+    return local.contiguous(), cu

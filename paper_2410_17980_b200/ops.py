@@ -171,20 +171,30 @@ def _params(q, scale, skip, skip_eps, block=DEFAULT_BLOCK, cu_seqlens=None,
 
 
 def _varlen_plan(cu_seqlens, q):
-    """Host copy of the offsets (one small D2H read) -> (lengths, max_seqlen)."""
+    """(host offsets, device offsets, lengths, max_seqlen).
+
+    The sizes of M, first_kb and the dZ workspace depend on every sequence
+    length, so the plan needs the offsets on the host: a CPU cu_seqlens is used
+    as is and uploaded without a stream sync (pinned staging copy); a device
+    cu_seqlens costs one small D2H read (which waits for the stream)."""
     if cu_seqlens.dtype != torch.int32 or cu_seqlens.dim() != 1 or cu_seqlens.numel() < 2:
         raise ValueError("cu_seqlens must be a 1-D int32 tensor of n_seq+1 offsets")
-    host = cu_seqlens.cpu()
+    if cu_seqlens.device.type == "cpu":
+        host = cu_seqlens.contiguous()
+        dev = host.pin_memory().to(q.device, non_blocking=True)
+    else:
+        host = cu_seqlens.cpu()
+        dev = cu_seqlens.to(device=q.device).contiguous()
     lens = (host[1:] - host[:-1]).tolist()
-    if host[0].item() != 0 or min(lens) < 0 or host[-1].item() != q.shape[0]:
+    if int(host[0]) != 0 or min(lens) < 0 or int(host[-1]) != q.shape[0]:
         raise ValueError("cu_seqlens must start at 0, be non-decreasing and end at total_tokens")
-    return host, lens, max(lens)
+    return host, dev, lens, max(lens)
 
 
 def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters):
     _check_qkv(q, k, v, varlen=True)
     T, H, d = q.shape
-    host, lens, max_L = _varlen_plan(cu_seqlens, q)
+    host, cu, lens, max_L = _varlen_plan(cu_seqlens, q)
     if skip_eps is None:
         skip_eps = default_skip_eps(q.dtype)
     if not 0.0 < skip_eps < 1.0:
@@ -192,7 +202,6 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     q, k, v = _same_layout(q, k, v)
-    cu = cu_seqlens.to(device=q.device, dtype=torch.int32).contiguous()
     lib = _lib.load()
     p = _params(q, scale, skip, skip_eps, cu_seqlens=cu, max_seqlen=max_L)
     n_snap, n_fkb = ctypes.c_size_t(), ctypes.c_size_t()

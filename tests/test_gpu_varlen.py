@@ -103,3 +103,17 @@ def test_varlen_skip_decisions_bit_exact():
         off += H * nb
         visited += ref["visited"]
     assert st.visited == visited
+
+
+def test_varlen_host_offsets_same_results():
+    """cu_seqlens on the host (no device sync to plan) gives the device-offsets results."""
+    import paper_2410_17980_b200 as sb
+    lens = [300, 77, 192, 1]
+    (q, k, v, d_o), cu = packed(lens, 2, 64, seed=9)
+    res = []
+    for c in (cu, cu.cpu()):
+        o, lr, _, cache = sb.blocked_forward(q, k, v, cu_seqlens=c)
+        res.append((o, lr) + tuple(sb.blocked_backward_twophase(cache, d_o)[:3]))
+    torch.cuda.synchronize()
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
