@@ -98,6 +98,13 @@ sb::Geom geom(const sb_params_t* p) {
   g.sh = p->stride_h;
   g.sl = p->stride_l;
   g.cu = p->cu_seqlens;
+  // grouped_order: units per group such that the group's K and V (bf16) fit a
+  // 32 MiB slice of the 126 MB L2, at least 8
+  // (varlen: the mean sequence length, so a group holds about as many tokens)
+  const int64_t len = (p->cu_seqlens && p->batch > 0) ? p->total_tokens / p->batch : p->seqlen;
+  const int64_t unit_bytes = 4 * std::max<int64_t>(1, len) * p->head_dim;
+  const int64_t bh = (int64_t)p->batch * p->heads;
+  g.ugroup = (int)std::max<int64_t>(1, std::min<int64_t>(bh, std::max<int64_t>(8, (32ll << 20) / unit_bytes)));
   return g;
 }
 

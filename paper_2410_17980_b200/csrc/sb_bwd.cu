@@ -186,7 +186,7 @@ __device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int 
                                         bool even_lo = false) {
   QItem it;
   int item, bh;
-  grouped_order(idx, (g.n_qt + 1) / 2, g.B * g.H, item, bh);
+  grouped_order(idx, (g.n_qt + 1) / 2, g.B * g.H, g.ugroup, item, bh);
   it.b = bh / g.H;
   it.h = bh % g.H;
   it.u = make_unit(g, it.b, it.h);
@@ -661,7 +661,7 @@ struct KVItem {
 __device__ __forceinline__ KVItem kv_item(const Geom& g, int idx) {
   KVItem it;
   int p, bh;
-  grouped_order(idx, (g.nb + 1) / 2, g.B * g.H, p, bh);
+  grouped_order(idx, (g.nb + 1) / 2, g.B * g.H, g.ugroup, p, bh);
   it.b = bh / g.H;
   it.h = bh % g.H;
   it.u = make_unit(g, it.b, it.h);

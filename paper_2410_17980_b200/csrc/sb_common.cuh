@@ -28,6 +28,7 @@ struct Geom {
   float scale_log2;         // softmax-free logit scale times log2(e)
   int64_t sb, sh, sl;       // element strides of q/k/v/o/do/dq/dk/dv (last dim contiguous)
   const int32_t* cu;        // varlen: [B+1] sequence offsets into the packed token axis
+  int ugroup;               // units per grouped_order group (host: L2 working-set budget)
 };
 
 // One (sequence, head) unit: its length and where its rows, snapshots and
@@ -96,17 +97,19 @@ __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
   return u;
 }
 
-// CTA -> (work item, unit): the CTAs of kUnitGroup units run together so that
-// the K/V (or Q/dO) stream each CTA reads is shared by its neighbours in L2 (a
-// unit's 4 x 1 MB inputs are re-read by every CTA of that unit); inside a group
-// item 0 (the heaviest, longest-processing-time first) goes first.
-constexpr int kUnitGroup = 8;
-__device__ __forceinline__ void grouped_order(int cta, int n_items, int BH, int& item, int& unit) {
-  const int grp = cta / (kUnitGroup * n_items);
-  const int rem = cta - grp * kUnitGroup * n_items;
-  const int gsz = min(kUnitGroup, BH - grp * kUnitGroup);
+// CTA -> (work item, unit): the CTAs of a group of g.ugroup units run together
+// so that the K/V (or Q/dO) stream each CTA reads is shared by its neighbours in
+// L2 (a unit's inputs are re-read by every CTA of that unit); inside a group
+// item 0 (the heaviest, longest-processing-time first) goes first.  The host
+// sizes groups to a fixed L2 budget (sb_api.cu), so a small problem (few units:
+// strong scaling, short varlen batches) is one group in global LPT order.
+__device__ __forceinline__ void grouped_order(int cta, int n_items, int BH, int ugroup, int& item,
+                                              int& unit) {
+  const int grp = cta / (ugroup * n_items);
+  const int rem = cta - grp * ugroup * n_items;
+  const int gsz = min(ugroup, BH - grp * ugroup);
   item = rem / gsz;
-  unit = grp * kUnitGroup + rem % gsz;
+  unit = grp * ugroup + rem % gsz;
 }
 
 // Dynamic work queue of the persistent kernels: the producer warp takes item

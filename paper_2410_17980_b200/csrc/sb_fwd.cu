@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(FwdCfg<D, NG>::kThreads, 1)
   // heavy-first schedule: the last query tiles have the longest key sweeps
   const int BH = g.B * g.H;
   int item, bh;
-  grouped_order((int)blockIdx.x, g.n_qt, BH, item, bh);
+  grouped_order((int)blockIdx.x, g.n_qt, BH, g.ugroup, item, bh);
   const int b = bh / g.H, h = bh % g.H;
   const Unit u = make_unit(g, b, h);
   if (item >= u.n_qt) return;  // shorter sequence of a varlen batch: no work

@@ -49,7 +49,7 @@ struct FwdItem {
 __device__ __forceinline__ FwdItem fwd_item(const Geom& g, int idx) {
   FwdItem it;
   int item, bh;
-  grouped_order(idx, (g.n_qt + 1) / 2, g.B * g.H, item, bh);
+  grouped_order(idx, (g.n_qt + 1) / 2, g.B * g.H, g.ugroup, item, bh);
   it.b = bh / g.H;
   it.h = bh % g.H;
   it.u = make_unit(g, it.b, it.h);
