@@ -45,6 +45,31 @@ def timed(fn, n=3):
     return a.elapsed_time(b) / n
 
 
+def margins(ref, L, eps, block=64):
+    """How close the oracle's skip decisions are to the threshold.
+
+    For every query block: the last visited tile passed the check with max_r a = max_r
+    M(qb, first_kb) >= log eps (margin a - log eps); a skipped tile (first_kb > 0) failed it
+    with max_r a = max_r log_rem < log eps (margin log eps - a).  Returns the minimum of each
+    and a histogram of all margins in decades (nats)."""
+    le = float(np.log(np.float32(eps)))
+    fkb, M, lr = ref["first_kb"], ref["M"], ref["log_rem"]
+    vis, skp = [], []
+    for u in range(fkb.shape[0]):
+        for qb in range(fkb.shape[1]):
+            rows = min(block, L - qb * block)
+            kb = int(fkb[u, qb])
+            vis.append(float(M[u, qb * (qb + 1) // 2 + kb, :rows].max()) - le)
+            if kb > 0:
+                skp.append(le - float(lr[u, qb * block: qb * block + rows].max()))
+    allm = np.array(vis + skp)
+    edges = [0, 1e-6, 1e-5, 1e-4, 1e-3, 1e-2, 1e-1, 1, np.inf]
+    hist = np.histogram(allm, bins=edges)[0].tolist()
+    return {"log_eps": le, "min_visit_margin": min(vis), "min_skip_margin": min(skp) if skp else None,
+            "hist_edges_nats": ["0", "1e-6", "1e-5", "1e-4", "1e-3", "1e-2", "0.1", "1", "inf"],
+            "hist": hist, "n_decisions": int(allm.size)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--B", type=int, default=1)
@@ -84,6 +109,7 @@ def main():
                                        block=64, skip=True, skip_eps=eps, dtype=np.float64)
             got = st.first_kb[0, :nh].cpu().numpy()
             entry["first_kb_bit_exact"] = bool(np.array_equal(got, ref["first_kb"]))
+            entry["decision_margins"] = margins(ref, a.L, eps)
             entry["oracle_heads_checked"] = nh
             entry["oracle_s"] = time.perf_counter() - t0
         elif name == "dead":
