@@ -1,6 +1,7 @@
 // C-ABI entry points (include/sb_attn.h): validation mirroring the reference's
 // ValueErrors, TMA tensor-map encoding and kernel dispatch.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <cudaTypedefs.h>
@@ -160,11 +161,16 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   a.log_eps = std::log(eps);
   a.trace = g_trace;
   a.sched = reinterpret_cast<unsigned*>(M);
-  // skip on: exact log-space kernel (bit-exact skip decisions); skip off: the
-  // ping-pong product-form kernel
+  // the persistent ping-pong product-form kernel, with the exact skip decisions
+  // when skip is on; SB_FWD_SKIP_V1=1 selects the older all-log-space skip kernel
+  // (sb_fwd.cu, kept as a cross-check)
   cudaStream_t st_ = reinterpret_cast<cudaStream_t>(stream);
-  int rc = p->skip ? sb::fwd_dispatch(p->head_dim, true, tq, tk, tv, a, st_)
-                   : sb::fwd_pp_dispatch(p->head_dim, tq, tk, tv, a, st_);
+  static const bool v1 = [] {
+    const char* e = std::getenv("SB_FWD_SKIP_V1");
+    return e && e[0] == '1';
+  }();
+  int rc = (p->skip && v1) ? sb::fwd_dispatch(p->head_dim, true, tq, tk, tv, a, st_)
+                           : sb::fwd_pp_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a, st_);
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
 

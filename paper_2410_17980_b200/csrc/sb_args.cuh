@@ -46,8 +46,8 @@ constexpr int kTraceCtas = 4;
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
                  const CUtensorMap& tv, const CUtensorMap& tz, const BwdArgs& a, int phases,
                  bool store, cudaStream_t stream);
-int fwd_pp_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                    const FwdArgs& a, cudaStream_t stream);
+int fwd_pp_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
+                    const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
 int fwd_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
                  const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
 

@@ -274,6 +274,66 @@ __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_
   return ok;
 }
 
+// Skip-on forward (sb_fwd_pp_kernel<D, true>): the row's exact sum of lt for the
+// skip decisions, with the exact-path kernel's arithmetic (log_pass + the group
+// totals added 0..3: per 16-column group, right to left, f32), and t = 2^Z left
+// in s[] for the product form (0 where masked).  Returns the sum in log2 units.
+template <bool kDiag>
+__device__ __forceinline__ float exact_lt_row(float* s, float scale_log2, int lim) {
+  float tot = 0.0f;
+#pragma unroll
+  for (int g = 0; g < kBlock / 16; ++g) {
+    float cum = 0.0f;
+#pragma unroll
+    for (int c = 15; c >= 0; --c) {
+      const int col = 16 * g + c;
+      const float Z = s[col] * scale_log2;
+      const float t = ex2(Z);
+      const float sp = softplus2(Z, t);
+      const bool m = !kDiag || col < lim;
+      cum -= m ? sp : 0.0f;
+      s[col] = m ? t : 0.0f;
+    }
+    tot += cum;
+  }
+  return tot;
+}
+
+// batched_row's product form from precomputed t (s[] = t, masked columns 0): A
+// into pk with Q = e^a carried right to left.  False if a group product reached
+// 2^64 (the caller redoes the row per element).
+__device__ __forceinline__ bool batched_from_t(const float* s, uint32_t* pk, float Q) {
+  constexpr int NG = kBlock / 16;
+  float P[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) P[g] = 1.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) P[g] = fmaf(P[g], s[16 * g + i], P[g]);
+  bool ok = true;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < kBatchedMax);
+  float F[NG];
+#pragma unroll
+  for (int g = NG - 1; g >= 0; --g) {
+    F[g] = Q * rcp(P[g]);
+    Q = F[g];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; i += 2)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int c = 16 * g + i;
+      const float a0 = s[c] * F[g];
+      F[g] = fmaf(F[g], s[c], F[g]);
+      const float a1 = s[c + 1] * F[g];
+      F[g] = fmaf(F[g], s[c + 1], F[g]);
+      pk[c >> 1] = pack_bf16(a0, a1);
+    }
+  return ok;
+}
+
 // Log-space variant (exact skip path, blocked.py:179-186 restated): Z on exit in
 // zs[c], inclusive in-group suffix sums of lt (log2 units) in cl[c]; returns the
 // group total. Branch-free: masked columns contribute 0.

@@ -32,9 +32,10 @@ struct FwdPPCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffP = kOffV + kStages * kKVBytes;       // P[wg][buf]
   static constexpr int kOffBar = kOffP + 4 * kPBytes;
-  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 8 + 2 + 2 + 1 + 8 + 2;
+  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 8 + 2 + 2 + 1 + 8 + 2 + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
-  static constexpr int kSmem = kOffMisc + 64 + 1024;
+  // misc: TMEM slot, work-queue ring, skip flags (+64), skip max exchange (+128)
+  static constexpr int kSmem = kOffMisc + 256 + 1024;
   // per WG w: S at w*128 (single-buffered), Q (MMA A operand) at w*128 + 64,
   // O at 256 + w*128
   static constexpr uint32_t kTmemCols = 512;
@@ -69,7 +70,15 @@ __device__ __forceinline__ FwdItem fwd_item(const Geom& g, int idx) {
 // across items; Q of the next item loads once the last S of the current item
 // was issued (q_free), and the next item's first A.V waits until the
 // warpgroup has read O out of TMEM (ofree).
-template <int D>
+// kSkip: block skipping (blocked.py:175-176) with the exact-path kernel's
+// decision arithmetic (f64 running `a` from f32 exact lt sums, max over each
+// 64-row query block before every tile), so first_kb is bit-exact against the
+// oracle.  Per element one more MUFU (lg2 of the exact softplus) than skip off.
+// A warpgroup whose two query blocks are both done publishes its stop (stream
+// tile count) before releasing S, so its issuer never issues the next S; the
+// producer stops loading once both warpgroups stopped and publishes how many
+// tiles it loaded (bar_nload), so each issuer can release the tail of the ring.
+template <int D, bool kSkip>
 __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     sb_fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const FwdArgs args) {
@@ -94,6 +103,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), bar_qfree + 1, bar_qfree + 5};
   uint64_t* bar_qtm = bar_qfree + 9;  // [2] the warpgroup copied its Q tile into TMEM
+  uint64_t* bar_nload = bar_qtm + 2;  // [2] (skip) the producer's tile count of an item
+  // skip: per warpgroup (seq << 13) | stop of its current item (-1: none yet), and
+  // per item parity the number of stream tiles the producer loaded
+  volatile int* wg_done = reinterpret_cast<volatile int*>(smem + C::kOffMisc + 64);
+  volatile int* nload_v = wg_done + 2;
+  double* red = reinterpret_cast<double*>(smem + C::kOffMisc + 128);  // [wg][parity][quarter]
+  auto stop_of = [&](int w, int seq) -> int {
+    const int v = wg_done[w];
+    return (v >> 13) == seq ? (v & 8191) : 0x7fffffff;
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
@@ -116,6 +135,9 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     mbar_init(bar_qfree, 2);
     mbar_init(bar_qtm, 128);
     mbar_init(bar_qtm + 1, 128);
+    mbar_init(bar_nload, 1);
+    mbar_init(bar_nload + 1, 1);
+    wg_done[0] = wg_done[1] = -1;
     sched_init(sq, 10);  // consumers: stick warps 0-7, issuer warps 9-10
     fence_mbar_init();
   }
@@ -149,9 +171,29 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
                         c * 64, u.trow0 + (2 * it.p + w) * kTileM, it.h, u.tb);
       }
       __syncwarp();
+      int n_load = it.n_s;
       for (int j = 0; j < it.n_s; ++j, ++jg) {
         const int s = jg % ST;
-        if (jg >= ST) mbar_wait(bar_kvempty + s, ((jg / ST) - 1) & 1);
+        if constexpr (kSkip) {
+          // stop once both warpgroups are done; poll while waiting for the slot (its
+          // release may depend on this item's tile count when they are)
+          bool stop = false;
+          const long long t0 = clock64();
+          for (;;) {
+            if (clock64() - t0 > (1ll << 33)) __trap();  // deadlock: fail loudly
+            if (j > 0 && stop_of(0, ni) <= j && (!it.has1 || stop_of(1, ni) <= j)) {
+              stop = true;
+              break;
+            }
+            if (jg < ST || mbar_test(bar_kvempty + s, ((jg / ST) - 1) & 1)) break;
+          }
+          if (stop) {
+            n_load = j;
+            break;
+          }
+        } else {
+          if (jg >= ST) mbar_wait(bar_kvempty + s, ((jg / ST) - 1) & 1);
+        }
         const int kb = it.kbhi1 - j;
         if (leader) {
           mbar_expect_tx(bar_kfull + s, C::kKVBytes);
@@ -162,6 +204,13 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           for (int c = 0; c < D / 64; ++c)
             tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
                         c * 64, u.trow0 + kb * kBlock, it.h, u.tb);
+        }
+        __syncwarp();
+      }
+      if constexpr (kSkip) {
+        if (leader) {
+          nload_v[ni & 1] = n_load;
+          mbar_arrive(bar_nload + (ni & 1));
         }
         __syncwarp();
       }
@@ -184,23 +233,54 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     const uint32_t tS = tbase + w * 128, tQ = tS + 64, tO = tbase + 256 + w * 128;
     const bool leader = elect_one();
     int jg = 0, ni = 0, ig = 0, nwi = 0;
+    // skip: release stream tiles j_from.. of item ni (this warpgroup no longer reads
+    // them) as they land, until the producer has published how many it loaded; the
+    // producer may need those slots back before it knows (the other warpgroup can
+    // still be sweeping).  Returns that count.
+    auto release_tail = [&](int j_from) -> int {
+      uint64_t* nb_bar = bar_nload + (ni & 1);
+      const uint32_t nb_par = (ni >> 1) & 1;
+      for (int j = j_from;; ++j) {
+        const int js = jg + j, s = js % ST;
+        const uint32_t par = (js / ST) & 1;
+        const long long t0 = clock64();
+        for (;;) {
+          // landed-test first, count second: if the count is not out yet, a landed
+          // tile cannot be the next item's (the producer publishes before loading it)
+          const bool kv = mbar_test(bar_kfull + s, par) && mbar_test(bar_vfull + s, par);
+          if (mbar_test(nb_bar, nb_par)) {
+            const int n = nload_v[ni & 1];
+            if (j >= n) return n;
+          }
+          if (kv) break;
+          if (clock64() - t0 > (1ll << 33)) __trap();  // deadlock: fail loudly
+        }
+        if (leader) mbar_arrive(bar_kvempty + s);
+        __syncwarp();
+      }
+    };
     for (int k = 0;; ++k) {
       const int idx = sched_consume(sq, k);
       if (idx < 0) break;
       const FwdItem it = fwd_item(g, idx);
       if (!it.valid) continue;
       if (w == 1 && !it.has1) {  // no tile for this warpgroup: release the stream
-        for (int j = 0; j < it.n_s; ++j) {
-          const int js = jg + j;
-          mbar_wait(bar_vfull + js % ST, (js / ST) & 1);
-          if (leader) mbar_arrive(bar_kvempty + js % ST);
-          __syncwarp();
+        int n_rel = it.n_s;
+        if constexpr (kSkip) {
+          n_rel = release_tail(0);
+        } else {
+          for (int j = 0; j < n_rel; ++j) {
+            const int js = jg + j;
+            mbar_wait(bar_vfull + js % ST, (js / ST) & 1);
+            if (leader) mbar_arrive(bar_kvempty + js % ST);
+            __syncwarp();
+          }
         }
         // (after a V of this item landed: the producer is past the previous
         // item's q_free phase, so this arrival counts for this item's phase)
         if (leader) mbar_arrive(bar_qfree);
         __syncwarp();
-        jg += it.n_s;
+        jg += n_rel;
         ++ni;
         continue;
       }
@@ -236,10 +316,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         if (leader) mbar_arrive(bar_kvempty + js % ST);
         __syncwarp();
       }
+      int n_proc = n_w;  // tiles this warpgroup processes (skip: up to its stop)
       for (int i = 0; i < n_w; ++i) {
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
-        mbar_wait(bar_kfull + s, (js / ST) & 1);
         if (gi >= 1) mbar_wait(sempty, (gi - 1) & 1);  // S is single-buffered
+        // skip: the warpgroup published its stop before releasing S of tile i-1
+        if (kSkip && i > 0 && stop_of(w, ni) <= j0 + i) {
+          n_proc = i;
+          break;
+        }
+        mbar_wait(bar_kfull + s, (js / ST) & 1);
         SB_TR(args, 2 + w, gi, 8);
         tc_fence_after();
         if (leader) {
@@ -254,11 +340,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         SB_TR(args, 2 + w, gi, 10);
         if (i >= 1) issue_pv(i - 1);
       }
-      issue_pv(n_w - 1);
+      issue_pv(n_proc - 1);
       if (leader) umma_commit(bar_ofull + w);
       __syncwarp();
-      jg += it.n_s;
-      ig += n_w;
+      if constexpr (kSkip) {
+        // release the loaded stream tiles this warpgroup no longer reads
+        jg += release_tail(j0 + n_proc);
+      } else {
+        jg += it.n_s;
+      }
+      ig += n_proc;
       ++ni;
       ++nwi;
     }
@@ -315,6 +406,13 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const int kbhi = w ? it.kbhi1 : it.kbhi0;
       const int n_w = kbhi + 1;
       float a2 = 0.0f;  // running log2 remaining mass
+      // skip: exact running a (natural log), the two query blocks' sweep state,
+      // and (thread (r & 63) == 0) the block's leftmost visited tile and count
+      double a_d = 0.0;
+      const int qb0 = 2 * qt, half = r >> 6;
+      bool act[2] = {qb0 < u.nb, qb0 + 1 < u.nb};
+      int lowest = my_qb, visited = 0, n_proc = n_w;
+      const int j0 = it.kbhi1 - kbhi;  // stream index of this warpgroup's first tile
       for (int i = 0; i < n_w; ++i) {
         const int kb = kbhi - i, gi = ig + i;
         if (tr) SB_TR(args, w, gi, 0);
@@ -329,18 +427,44 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         bool slow = false;
         const bool diag = kb == my_qb;
         const int lim = diag ? (r & 63) : kBlock;
-        if (kb <= my_qb) {  // warp-uniform: a warp's rows share one 64-row half
-          // batched reciprocal (sb_common.cuh): one rcp per 16 columns
-          float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
-          slow = diag ? !batched_row<true>(s, pk, sl2, lim, Q, Dhi, Dlo)
-                      : !batched_row<false>(s, pk, sl2, kBlock, Q, Dhi, Dlo);
-          if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
-          if (!slow) a2 -= lg2(Dhi) + lg2(Dlo);
+        const float a2_in = a2;
+        // warp-uniform: a warp's rows share one 64-row half
+        if ((!kSkip || act[half]) && kb <= my_qb) {
+          if constexpr (kSkip) {
+            // exact lt sum first (t left in s[]), then the product form from t
+            const float tot = diag ? exact_lt_row<true>(s, sl2, lim) : exact_lt_row<false>(s, sl2, lim);
+            slow = !batched_from_t(s, pk, ex2(a2));
+            if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
+            a_d += (double)tot * (double)kLn2;
+            a2 = (float)(a_d * 1.4426950408889634);
+            lowest = kb;
+            ++visited;
+          } else {
+            // batched reciprocal (sb_common.cuh): one rcp per 16 columns
+            float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
+            slow = diag ? !batched_row<true>(s, pk, sl2, lim, Q, Dhi, Dlo)
+                        : !batched_row<false>(s, pk, sl2, kBlock, Q, Dhi, Dlo);
+            if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
+            if (!slow) a2 -= lg2(Dhi) + lg2(Dlo);
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
         }
-        if (__any_sync(0xffffffffu, slow)) {
+        if (kSkip && __any_sync(0xffffffffu, slow)) {
+          // a group product reached 2^64: per-element product form from t (a is exact)
+          if (slow) {
+            float Ql = ex2(a2_in), an = 0.0f;
+#pragma unroll
+            for (int c = kBlock - 1; c >= 0; --c) {
+              const float rr = rcp(1.0f + s[c]);
+              const float a = fminf(s[c] * rr, 1.0f) * Ql;  // t = inf: sigma = 1
+              Ql *= rr;
+              if (c & 1) an = a;
+              else pk[c >> 1] = pack_bf16(a, an);
+            }
+          }
+        } else if (!kSkip && __any_sync(0xffffffffu, slow)) {
           // a group product of (1+t) reached 2^64: per-element path for those rows
           // (S is still in TMEM: s_empty not yet signalled)
           tmem_ld32(tS, s);
@@ -369,6 +493,30 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             a2 += lt;
           }
         }
+        bool done = false;
+        if constexpr (kSkip) {
+          // skip check for the next tile (blocked.py:175-176) on a after this one:
+          // max over each 64-row query block, exchanged between its two warps
+          if (i + 1 < n_w) {
+            double m = row_valid ? a_d : -INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            double* rw = red + (w * 2 + (gi & 1)) * 4;
+            if (lane == 0) rw[quarter] = m;
+            named_bar_sync(1 + w, 128);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const double mh = fmax(rw[2 * hh], rw[2 * hh + 1]);
+              if (act[hh] && kb - 1 < qb0 + hh && mh < args.log_eps) act[hh] = false;
+            }
+            done = !act[0] && !act[1];
+            if (done) {
+              n_proc = i + 1;
+              // published before S is released: the issuer checks it before S(i+1)
+              if (r == 0) wg_done[w] = ((ni - 1) << 13) | (j0 + i + 1);
+            }
+          }
+        }
         tc_fence_before();
         mbar_arrive(sempty);  // S(i+1) may overwrite the buffer now
         if (tr) SB_TR(args, w, gi, 2);
@@ -382,6 +530,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         fence_proxy_async_smem();
         mbar_arrive(pfull + (gi & 1));
         if (tr) SB_TR(args, w, gi, 4);
+        if (done) break;
       }
       // epilogue: O rows leave in 64-column halves through this warp's 4 KB slice
       // of the (now idle: ofull) P buffers as coalesced row segments
@@ -403,12 +552,13 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         warp_store_rows<8>(ov, 1.0f, stage, args.o + u.out_off + (int64_t)row0 * g.sl + c * 64,
                            g.sl, nvalid);
       }
-      if (row_valid) args.log_rem[u.rem_off + row * u.rem_stride] = a2 * kLn2;
+      if (row_valid) args.log_rem[u.rem_off + row * u.rem_stride] = kSkip ? (float)a_d : a2 * kLn2;
       if (my_qb < u.nb && (r & 63) == 0) {
-        args.first_kb[u.fkb_off + my_qb] = 0;
-        if (args.counters) atomicAdd(args.counters, (unsigned long long)(my_qb + 1));
+        args.first_kb[u.fkb_off + my_qb] = kSkip ? lowest : 0;
+        if (args.counters)
+          atomicAdd(args.counters, (unsigned long long)(kSkip ? visited : my_qb + 1));
       }
-      ig += n_w;
+      ig += n_proc;
       ++nwi;
     }
   }
@@ -417,11 +567,11 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   if (warp == 8) tmem_dealloc<C::kTmemCols>(tbase);
 }
 
-template <int D>
+template <int D, bool kSkip>
 static int launch_fwd_pp(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          const FwdArgs& a, cudaStream_t stream) {
   using C = FwdPPCfg<D>;
-  auto kern = sb_fwd_pp_kernel<D>;
+  auto kern = sb_fwd_pp_kernel<D, kSkip>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return (int)e;
   if ((e = cudaMemsetAsync(a.sched, 0, sizeof(unsigned), stream)) != cudaSuccess) return (int)e;
@@ -435,10 +585,12 @@ static int launch_fwd_pp(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   return (int)cudaGetLastError();
 }
 
-int fwd_pp_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                    const FwdArgs& a, cudaStream_t stream) {
-  if (D == 128) return launch_fwd_pp<128>(tq, tk, tv, a, stream);
-  if (D == 64) return launch_fwd_pp<64>(tq, tk, tv, a, stream);
+int fwd_pp_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
+                    const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream) {
+  if (D == 128) return skip ? launch_fwd_pp<128, true>(tq, tk, tv, a, stream)
+                            : launch_fwd_pp<128, false>(tq, tk, tv, a, stream);
+  if (D == 64) return skip ? launch_fwd_pp<64, true>(tq, tk, tv, a, stream)
+                           : launch_fwd_pp<64, false>(tq, tk, tv, a, stream);
   return -1;
 }
 
