@@ -1449,6 +1449,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         LiveQt peek = it;
         Ma1 = Mbase[tix(peek.next())];
       }
+      if (tr) SB_TR(args, w, ni, 12);
       for (; qt < u.n_qt; ++jg) {
         const int my_qb = 2 * qt + (r >> 6);
         const uint32_t tSw = tSw0 + (jg & 1) * 128;
@@ -1515,6 +1516,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (any) {
         mbar_wait(done, ni & 1);
         if (tr && ni == 0) SB_TR(args, w, 0, 15);
+        if (tr) SB_TR(args, w, ni, 9);
         tc_fence_after();
       }
       {
@@ -1534,12 +1536,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
             for (int c = 0; c < HD; ++c) a[c] = 0.0f;
           }
+          if (tr && t == 0) SB_TR(args, w, ni, 13);
           if (t == 1 && any) {
             tc_fence_before();
             mbar_arrive(acc_free);  // the next item's dV/dK may start
           }
           __nv_bfloat16* dst = (t ? args.dk : args.dv) + u.out_off + (int64_t)key0 * g.sl + w * HD;
           warp_store_rows<HD / 8>(a, t ? scale : 1.0f, stage, dst, g.sl, nvalid);
+          if (tr) SB_TR(args, w, ni, 10 + t);
         }
       }
       if (any) ++ni;
