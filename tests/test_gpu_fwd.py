@@ -87,3 +87,38 @@ def test_bshd_layout():
     assert qs.stride() != q.stride()
     o, *_ = sb.blocked_forward(qs, ks, vs)
     assert torch.equal(o.contiguous(), o_ref)
+
+
+_V1_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2410_17980_b200 as sb
+from tests.gpu_util import make_qkv
+q, k, v, _ = make_qkv(1, 8, 4096, 128, seed=7, family="shift", mu=-6.0)
+o, lr, st, _ = sb.blocked_forward(q, k, v, skip=True, skip_eps=1e-6)
+torch.cuda.synchronize()
+np.savez(sys.argv[2], first_kb=st.first_kb.cpu().numpy(), visited=st.visited,
+         o=o.float().cpu().numpy(), log_rem=lr.cpu().numpy())
+"""
+
+
+def test_skip_kernels_agree(tmp_path):
+    """The persistent skip-on forward and the older all-log-space skip kernel
+    (SB_FWD_SKIP_V1=1, selected once per process) make the same skip decisions on
+    8 heads of the tight-margin mu = -6 family, and agree on o / log_rem."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for v1 in ("0", "1"):
+        out = tmp_path / f"v{v1}.npz"
+        env = dict(os.environ, SB_FWD_SKIP_V1=v1)
+        subprocess.run([sys.executable, "-c", _V1_SCRIPT, root, str(out)], env=env, check=True,
+                       cwd=root, timeout=300)
+        res.append(np.load(out))
+    a, b = res
+    np.testing.assert_array_equal(a["first_kb"], b["first_kb"])
+    assert int(a["visited"]) == int(b["visited"]) < 8 * 64 * 65 // 2
+    assert np.max(np.abs(a["o"] - b["o"])) / max(1.0, np.max(np.abs(b["o"]))) < 2e-2
+    assert np.max(np.abs(a["log_rem"] - b["log_rem"])) < 1e-3 * max(1.0, np.max(np.abs(b["log_rem"])))
