@@ -160,7 +160,8 @@ template <int D>
 struct BwdQCfg {
   // K ring of 3 stages (S(j) and dQ(j) read K(j): released at the end of tile j);
   // V single-buffered (only dW(j) reads V(j): released early in tile j).
-  static constexpr int kStages = 3;
+  static constexpr int kStages = 3;   // K ring
+  static constexpr int kVStages = 1;  // V ring (its own producer warp)
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kKVBytes = kBlock * D * 2;
   static constexpr int kZBytes = kTileM * kBlock * 2;
@@ -168,9 +169,9 @@ struct BwdQCfg {
   static constexpr int kOffDO = kOffQ + 2 * kQBytes;    // dO[2]
   static constexpr int kOffK = kOffDO + 2 * kQBytes;    // K ring
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
-  static constexpr int kOffZ = kOffV + kKVBytes;        // Z[2] (one per WG)
+  static constexpr int kOffZ = kOffV + kVStages * kKVBytes;  // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 * 8 + 1 + 8;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_z, const BwdArgs args) {
   using C = BwdQCfg<D>;
-  constexpr int ST = C::kStages;
+  constexpr int ST = C::kStages, VST = C::kVStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -234,8 +235,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_kfull = bars + 1;
   uint64_t* bar_kempty = bar_kfull + ST;
   uint64_t* bar_vfull = bar_kempty + ST;
-  uint64_t* bar_vempty = bar_vfull + 1;
-  uint64_t* wgbars = bar_vempty + 1;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done, dq_free
+  uint64_t* bar_vempty = bar_vfull + VST;
+  uint64_t* wgbars = bar_vempty + VST;  // per wg: sfull, sempty, wfull, wempty, zfull, zempty, done, dq_free
   uint64_t* bar_qdofree = wgbars + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), bar_qdofree + 1,
@@ -247,8 +248,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(bar_kfull + s, 1);
       mbar_init(bar_kempty + s, 2);  // one arrival per warpgroup issuer (dQ read K)
     }
-    mbar_init(bar_vfull, 1);
-    mbar_init(bar_vempty, 2);  // one arrival per warpgroup issuer (dW read V)
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(bar_vfull + s, 1);
+      mbar_init(bar_vempty + s, 2);  // one arrival per warpgroup issuer (dW read V)
+    }
     for (int w = 0; w < 2; ++w) {
       mbar_init(wgbars + w * 8 + 0, 1);    // sfull: S = Q K^T landed in TMEM
       mbar_init(wgbars + w * 8 + 1, 128);  // sempty: S read into registers
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(wgbars + w * 8 + 7, 128);  // dq_free: dQ read out of TMEM
     }
     mbar_init(bar_qdofree, 2);
-    sched_init(sq, 10);  // consumers: stick warps 0-7, issuer warps 9-10
+    sched_init(sq, 11);  // consumers: stick warps 0-7, issuer warps 9-10, V producer 11
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -314,16 +317,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                           u.trow0 + kb * kBlock, it.h, u.tb);
           }
           __syncwarp();
-          if (jg >= 1) mbar_wait(bar_vempty, (jg - 1) & 1);
+        }
+        ++ni;
+      }
+    } else if (warp == 11) {
+      // ---------------------------------------------------------- V producer: its ring
+      // is released early (dW reads V), so it runs ahead of the K ring's producer
+      const bool leader = elect_one();
+      int jg = 0;
+      for (int kq = 0;; ++kq) {
+        const int idx = sched_consume(sq, kq);
+        if (idx < 0) break;
+        const QItem it = q_item(g, args.first_kb, idx, kStoreZ);
+        if (!it.valid) continue;
+        const Unit& u = it.u;
+        for (int j = 0; j < it.n_s; ++j, ++jg) {
+          const int s = jg % VST;
+          if (jg >= VST) mbar_wait(bar_vempty + s, ((jg / VST) - 1) & 1);
           if (leader) {
-            mbar_expect_tx(bar_vfull, C::kKVBytes);
+            mbar_expect_tx(bar_vfull + s, C::kKVBytes);
             for (int c = 0; c < D / 64; ++c)
-              tma_load_4d(&tm_v, bar_vfull, smem + C::kOffV + c * (kBlock * 128), c * 64,
-                          u.trow0 + kb * kBlock, it.h, u.tb);
+              tma_load_4d(&tm_v, bar_vfull + s, smem + C::kOffV + s * C::kKVBytes + c * (kBlock * 128),
+                          c * 64, u.trow0 + (it.kb_lo + j) * kBlock, it.h, u.tb);
           }
           __syncwarp();
         }
-        ++ni;
       }
     } else if (warp == 9 || warp == 10) {
       // ---------------------------------------------------------- MMA issuer of one WG
@@ -353,8 +371,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int js = jg + j;
             mbar_wait(bar_kfull + js % ST, (js / ST) & 1);
             if (leader) mbar_arrive(bar_kempty + js % ST);
-            mbar_wait(bar_vfull, js & 1);
-            if (leader) mbar_arrive(bar_vempty);
+            mbar_wait(bar_vfull + js % VST, (js / VST) & 1);
+            if (leader) mbar_arrive(bar_vempty + js % VST);
             __syncwarp();
           }
           // (after a K of this item landed: the producer is past the previous
@@ -389,8 +407,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
         };
         auto issue_w = [&](int j) {
-          const int js = jg + j, gi = ig + j;
-          mbar_wait(bar_vfull, js & 1);
+          const int js = jg + j, gi = ig + j, sv = js % VST;
+          mbar_wait(bar_vfull + sv, (js / VST) & 1);
           if (gi >= 1) mbar_wait(wempty, (gi - 1) & 1);
           SB_TR(args, 2 + w, gi, 10);
           tc_fence_after();
@@ -399,10 +417,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             for (int k = 0; k < D / 16; ++k) {
               const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
               const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-              umma_ss_at(tW, ddo, off, dv, offk, idesc_s, k > 0);
+              umma_ss_at(tW, ddo, off, dv, sv * C::kKVBytes + offk, idesc_s, k > 0);
             }
             umma_commit(wfull);
-            umma_commit(bar_vempty);
+            umma_commit(bar_vempty + sv);
             if (j + 1 == n_w) umma_commit(bar_qdofree);  // Q and dO read for the last time
           }
           __syncwarp();
@@ -446,8 +464,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int js = jg + j;
           mbar_wait(bar_kfull + js % ST, (js / ST) & 1);
           if (leader) mbar_arrive(bar_kempty + js % ST);
-          mbar_wait(bar_vfull, js & 1);
-          if (leader) mbar_arrive(bar_vempty);
+          mbar_wait(bar_vfull + js % VST, (js / VST) & 1);
+          if (leader) mbar_arrive(bar_vempty + js % VST);
           __syncwarp();
         }
         jg += it.n_s;
