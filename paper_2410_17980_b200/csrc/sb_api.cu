@@ -217,10 +217,9 @@ int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v,
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(d_o) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return SB_ERR_UNSUPPORTED;
-  CUtensorMap tq, tdo, tk, tv, tz, tdk, tdv;
+  CUtensorMap tq, tdo, tk, tv, tz;
   if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
-      (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)) ||
-      (st = make_map(&tdk, dk, p, 32)) || (st = make_map(&tdv, dv, p, 32)))
+      (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)))
     return st;
   const bool store = ztiles != nullptr;
   std::memset(&tz, 0, sizeof(tz));
@@ -240,7 +239,7 @@ int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v,
   a.N = N;
   a.trace = g_trace;
   a.sched = reinterpret_cast<unsigned*>(N);
-  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, tdk, tdv, a, phases, store,
+  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, a, phases, store,
                             reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }

@@ -44,9 +44,8 @@ constexpr int kTraceCtas = 4;
 
 // store = dZ tile workspace mode (tz maps it; phase 1 writes, phase 2 reads)
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                 const CUtensorMap& tv, const CUtensorMap& tz, const CUtensorMap& tdk,
-                 const CUtensorMap& tdv, const BwdArgs& a, int phases, bool store,
-                 cudaStream_t stream);
+                 const CUtensorMap& tv, const CUtensorMap& tz, const BwdArgs& a, int phases,
+                 bool store, cudaStream_t stream);
 int fwd_pp_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
 int fwd_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,

@@ -1190,7 +1190,6 @@ template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     sb_bwd_kvs_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                       const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_z,
-                      const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
                       const BwdArgs args) {
   using C = BwdKVSCfg<D>;
   constexpr int ST = C::kStages;
@@ -1560,36 +1559,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_before();
             mbar_arrive(acc_free);  // the next item's dV/dK may start
           }
-          if (D == 128 && nvalid == 32) {
-            // whole 32-key x 64-column box: stage it and let the TMA write it out, so
-            // the warpgroup is not held by the global stores at the item boundary
-            if (t == 1) {  // dV's store has finished reading the stage
-              if (lane == 0) bulk_wait_read0();
-              __syncwarp();
-            }
-            warp_stage_rows<HD / 8>(a, t ? scale : 1.0f, stage);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_4d(t ? &tm_dk : &tm_dv, smem + C::kOffA + (warp & 7) * (32 * HD * 2),
-                           w * HD, u.trow0 + key0, wi.h, u.tb);
-              bulk_commit();
-            }
-            __syncwarp();
-          } else {
-            __nv_bfloat16* dst = (t ? args.dk : args.dv) + u.out_off + (int64_t)key0 * g.sl + w * HD;
-            warp_store_rows<HD / 8>(a, t ? scale : 1.0f, stage, dst, g.sl, nvalid);
-          }
+          __nv_bfloat16* dst = (t ? args.dk : args.dv) + u.out_off + (int64_t)key0 * g.sl + w * HD;
+          warp_store_rows<HD / 8>(a, t ? scale : 1.0f, stage, dst, g.sl, nvalid);
           if (tr) SB_TR(args, w, ni, 10 + t);
         }
-        // the stage is this warp's rows of the A buffers: the next item writes them
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
       }
       if (any) ++ni;
     }
-    if (lane == 0) bulk_wait0();  // the dK/dV tensor stores are complete
-    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -1598,9 +1574,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 template <int D>
 static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                      const CUtensorMap& tv, const CUtensorMap& tz, const CUtensorMap& tdk,
-                      const CUtensorMap& tdv, const BwdArgs& a, int phases, bool store,
-                      cudaStream_t stream) {
+                      const CUtensorMap& tv, const CUtensorMap& tz, const BwdArgs& a, int phases,
+                      bool store, cudaStream_t stream) {
   const unsigned BH = (unsigned)(a.g.B * a.g.H);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1627,7 +1602,7 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
       auto kern = sb_bwd_kvs_kernel<D>;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
       if (e != cudaSuccess) return (int)e;
-      kern<<<grid, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tz, tdk, tdv, a);
+      kern<<<grid, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tz, a);
     } else {
       using C = BwdKVCfg<D>;
       auto kern = sb_bwd_kv_kernel<D>;
@@ -1643,11 +1618,10 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
 }
 
 int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
-                 const CUtensorMap& tv, const CUtensorMap& tz, const CUtensorMap& tdk,
-                 const CUtensorMap& tdv, const BwdArgs& a, int phases, bool store,
-                 cudaStream_t stream) {
-  if (D == 128) return launch_bwd<128>(tq, tdo, tk, tv, tz, tdk, tdv, a, phases, store, stream);
-  if (D == 64) return launch_bwd<64>(tq, tdo, tk, tv, tz, tdk, tdv, a, phases, store, stream);
+                 const CUtensorMap& tv, const CUtensorMap& tz, const BwdArgs& a, int phases,
+                 bool store, cudaStream_t stream) {
+  if (D == 128) return launch_bwd<128>(tq, tdo, tk, tv, tz, a, phases, store, stream);
+  if (D == 64) return launch_bwd<64>(tq, tdo, tk, tv, tz, a, phases, store, stream);
   return -1;
 }
 

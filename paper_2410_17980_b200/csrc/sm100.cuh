@@ -99,14 +99,6 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* src, int c0, int c1,
-                                             int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-          reinterpret_cast<uint64_t>(m)),
-      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1,
                                              int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::
@@ -345,22 +337,6 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
                : "r"(addr)
                : "memory");
   return v;
-}
-
-// The staging half of warp_store_rows: 32 rows (lane = row) of NCH 16-byte chunks,
-// bf16(v * mul), 16-byte chunks XOR-swizzled by row (with NCH = 8 this is the TMA
-// 128B-swizzle image of a 32 x 64 bf16 box when stage is 1024-byte aligned).
-template <int NCH>
-__device__ __forceinline__ void warp_stage_rows(const float* v, float mul, uint32_t stage) {
-  const int lane = threadIdx.x & 31;
-  constexpr int RB = NCH * 16;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c)
-    st_shared_v4(stage + lane * RB + ((c ^ (lane & (NCH - 1))) << 4),
-                 pack_bf16(v[8 * c] * mul, v[8 * c + 1] * mul),
-                 pack_bf16(v[8 * c + 2] * mul, v[8 * c + 3] * mul),
-                 pack_bf16(v[8 * c + 4] * mul, v[8 * c + 5] * mul),
-                 pack_bf16(v[8 * c + 6] * mul, v[8 * c + 7] * mul));
 }
 
 // Coalesced store of a warp's 32 rows (lane j holds row j: NCH*8 floats, times
