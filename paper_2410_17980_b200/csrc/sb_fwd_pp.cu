@@ -471,24 +471,41 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           tmem_ld32(tS + 32, s + 32);
           tmem_wait_ld();
           if (slow) {
-            // per-element product form for A, exact softplus sum for a
+            // per-element product form for A; the row's lt from each 16-column
+            // group's product of r (one lg2 per group), or the exact softplus sum
+            // for a group whose product leaves the normal range or holds a logit
+            // beyond the clamp (2 MUFU per element instead of 3)
             float Ql = ex2(a2), lt = 0.0f;
 #pragma unroll
-            for (int c = kBlock - 1; c >= 0; c -= 2) {
-              float A[2];
+            for (int g = kBlock / 16 - 1; g >= 0; --g) {
+              float pr = 1.0f;
+              bool big = false;
 #pragma unroll
-              for (int uu = 0; uu < 2; ++uu) {
-                const int cc = c - uu;
-                const float Z = fminf(s[cc] * sl2, 126.0f);  // t finite: sigma = t*r <= 1
-                const float t = ex2(Z);
-                float rr = rcp(1.0f + t), sg = t * rr;
-                const float sp = softplus2(s[cc] * sl2, t);
-                if (cc >= lim) { rr = 1.0f; sg = 0.0f; }
-                lt -= (cc < lim) ? sp : 0.0f;
-                A[uu] = sg * Ql;
-                Ql *= rr;
+              for (int c = 16 * g + 15; c >= 16 * g; c -= 2) {
+                float A[2];
+#pragma unroll
+                for (int uu = 0; uu < 2; ++uu) {
+                  const int cc = c - uu;
+                  const float Zr = s[cc] * sl2;
+                  big = big || (Zr > 126.0f && cc < lim);
+                  const float t = ex2(fminf(Zr, 126.0f));  // t finite: sigma = t*r <= 1
+                  float rr = rcp(1.0f + t), sg = t * rr;
+                  if (cc >= lim) { rr = 1.0f; sg = 0.0f; }
+                  A[uu] = sg * Ql;
+                  Ql *= rr;
+                  pr *= rr;
+                }
+                pk[(c - 1) >> 1] = pack_bf16(A[1], A[0]);
               }
-              pk[(c - 1) >> 1] = pack_bf16(A[1], A[0]);
+              if (!big && pr >= kProdFloor) {
+                lt += lg2(pr);
+              } else {
+#pragma unroll
+                for (int cc = 16 * g; cc < 16 * g + 16; ++cc) {
+                  const float Zr = s[cc] * sl2;
+                  lt -= (cc < lim) ? softplus2(Zr, ex2(fminf(Zr, 126.0f))) : 0.0f;
+                }
+              }
             }
             a2 += lt;
           }

@@ -122,3 +122,20 @@ def test_skip_kernels_agree(tmp_path):
     assert int(a["visited"]) == int(b["visited"]) < 8 * 64 * 65 // 2
     assert np.max(np.abs(a["o"] - b["o"])) / max(1.0, np.max(np.abs(b["o"]))) < 2e-2
     assert np.max(np.abs(a["log_rem"] - b["log_rem"])) < 1e-3 * max(1.0, np.max(np.abs(b["log_rem"])))
+
+
+@pytest.mark.parametrize("family,mu,L,d", [("saturating", 0.0, 512, 128), ("shift", 8.0, 384, 64),
+                                           ("shift", 100.0, 256, 128), ("saturating", 0.0, 200, 64)])
+def test_large_logits_skip_off(family, mu, L, d):
+    """Skip off with group products beyond 2^64 (the per-element path): o and log_rem
+    vs the oracle, including logits past the exp2 clamp (mu = 100: z ~ 100 nats)."""
+    import paper_2410_17980_b200 as sb
+    q, k, v = make_qkv(1, 2, L, d, seed=5, family=family, mu=mu, with_do=False)
+    o, log_rem, _, _ = sb.blocked_forward(q, k, v, skip=False)
+    torch.cuda.synchronize()
+    ref = oracle_fwd(q, k, v)
+    err_o = rel_to_max(to64(o), ref["o"])
+    err_a = max_rel_err(to64(log_rem), ref["log_rem"])
+    print(f"{family} mu{mu} L{L} d{d}: o {err_o:.3e} log_rem {err_a:.3e}")
+    assert err_o < TOL
+    assert err_a < TOL
