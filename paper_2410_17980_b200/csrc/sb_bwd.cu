@@ -75,7 +75,7 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
   bool ok = true;
 #pragma unroll
   for (int g = 0; g < NG; ++g) ok = ok && (tot[g] < kBatchedMax);
-  if (ok) {
+  auto fast = [&]() {
     float inv[NG], K[NG];
     float Q = E;
 #pragma unroll
@@ -95,16 +95,31 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
         s[c] = u * K[g];
         if (kSigma) inv[g] = fmaf(inv[g], t, inv[g]);
       }
+  };
+  if (ok) {
+    fast();
   } else {
-    float Q = E;
+    // the wider range (sb_common.cuh), with the fast path's seed arithmetic
+    bool wide = true;
+    float k0 = E;
 #pragma unroll
-    for (int c = kBlock - 1; c >= 0; --c) {
-      const float t = s[c];
-      const float r = rcp(1.0f + t);
-      const float sgm = fminf(t * r, 1.0f);  // t = inf: NaN -> 1
-      s[c] = sgm * Q;
-      sg[c] = sgm;
-      Q *= r;
+    for (int g = NG - 1; g >= 0; --g) {
+      wide = wide && (tot[g] < kBatchedWide);
+      k0 = k0 * rcp(tot[g]);
+    }
+    if (wide && batched_seed_ok(k0, E)) {
+      fast();
+    } else {
+      float Q = E;
+#pragma unroll
+      for (int c = kBlock - 1; c >= 0; --c) {
+        const float t = s[c];
+        const float r = rcp(1.0f + t);
+        const float sgm = fminf(t * r, 1.0f);  // t = inf: NaN -> 1
+        s[c] = sgm * Q;
+        sg[c] = sgm;
+        Q *= r;
+      }
     }
   }
 }
@@ -1486,25 +1501,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const bool ok = diag ? recompute_a_pipe<true>(sv, pk, g.scale_log2, E, r & 63)
                              : recompute_a_pipe<false>(sv, pk, g.scale_log2, E, kBlock);
         if (__any_sync(0xffffffffu, !ok)) {
-          // a group product of (1+t) reached 2^64: recompute_row's per-element
-          // path for those rows (t recomputed from S, identically)
+          // outside the 2^64 range: recompute_row (wider-range retry, else one rcp
+          // per element) on S reloaded for those rows, as the recompute-mode kernel
           tmem_ld32(tSw, sv);
           tmem_ld32(tSw + 32, sv + 32);
           tmem_wait_ld();
           if (!ok) {
-            const int lim = diag ? (r & 63) : kBlock;
-            float Ql = E, an = 0.0f;
+            float sg[64];
+            if (diag) recompute_row<true, false>(sv, sg, g.scale_log2, E, r & 63);
+            else recompute_row<false, false>(sv, sg, g.scale_log2, E, kBlock);
 #pragma unroll
-            for (int c = kBlock - 1; c >= 0; --c) {
-              float t = ex2(sv[c] * g.scale_log2);
-              if (c >= lim) t = 0.0f;
-              const float rr = rcp(1.0f + t);
-              const float sgm = fminf(t * rr, 1.0f);
-              const float a = sgm * Ql;
-              Ql *= rr;
-              if (c & 1) an = a;
-              else pk[c >> 1] = pack_bf16(a, an);
-            }
+            for (int i = 0; i < 32; ++i) pk[i] = pack_bf16(sv[2 * i], sv[2 * i + 1]);
           }
         }
         tc_fence_before();

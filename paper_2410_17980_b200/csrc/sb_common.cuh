@@ -222,6 +222,17 @@ __device__ __forceinline__ float prod_pass(float* zs, float* w, float* sg, float
 // s[] is overwritten with t (the caller reloads S for the slow path).
 // Masked columns (c >= lim, diagonal tiles only) get t = 0: A = 0, r = 1.
 constexpr float kBatchedMax = 1.8446744073709552e19f;  // 2^64
+// Wider range, tried only on a row that failed the 2^64 check (large logits), in
+// the rare slow branch so the common path is unchanged: the batched form stays
+// exact while every group product is < 2^126 (its rcp is normal) and the smallest
+// group seed (carry / product) does not underflow, or the carried mass is
+// negligible (below 2^-100 every A of the row is too).
+constexpr float kBatchedWide = 8.507059173023462e37f;  // 2^126
+constexpr float kSeedMin = 2.350988701644575e-38f;     // 2^-125
+constexpr float kMassNeg = 7.888609052210118e-31f;     // 2^-100
+__device__ __forceinline__ bool batched_seed_ok(float seed_min, float q_in) {
+  return seed_min >= kSeedMin || q_in < kMassNeg;
+}
 
 template <bool kDiag>
 __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_log2, int lim,
@@ -274,6 +285,51 @@ __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_
   return ok;
 }
 
+// batched_row in the wider range (slow branch of the skip-off forward): s[] = raw S
+// on entry.  On success pk holds A and lsum the row's log2 product of (1+t).
+template <bool kDiag>
+__device__ __forceinline__ bool batched_row_wide(float* s, uint32_t* pk, float scale_log2, int lim,
+                                                 float Q, float& lsum) {
+  constexpr int NG = kBlock / 16;
+  const float q_in = Q;
+  float P[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) P[g] = 1.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int c = 16 * g + i;
+      float tt = ex2(s[c] * scale_log2);
+      if (kDiag) tt = c < lim ? tt : 0.0f;
+      s[c] = tt;
+      P[g] = fmaf(P[g], tt, P[g]);
+    }
+  bool ok = true;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < kBatchedWide);
+  float F[NG];
+#pragma unroll
+  for (int g = NG - 1; g >= 0; --g) {
+    F[g] = Q * rcp(P[g]);
+    Q = F[g];
+  }
+  if (!(ok && batched_seed_ok(Q, q_in))) return false;
+#pragma unroll
+  for (int i = 0; i < 16; i += 2)
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const int c = 16 * g + i;
+      const float a0 = s[c] * F[g];
+      F[g] = fmaf(F[g], s[c], F[g]);
+      const float a1 = s[c + 1] * F[g];
+      F[g] = fmaf(F[g], s[c + 1], F[g]);
+      pk[c >> 1] = pack_bf16(a0, a1);
+    }
+  lsum = (lg2(P[3]) + lg2(P[2])) + (lg2(P[1]) + lg2(P[0]));
+  return true;
+}
+
 // Skip-on forward (sb_fwd_pp_kernel<D, true>): the row's exact sum of lt for the
 // skip decisions, with the exact-path kernel's arithmetic (log_pass + the group
 // totals added 0..3: per 16-column group, right to left, f32), and t = 2^Z left
@@ -302,7 +358,9 @@ __device__ __forceinline__ float exact_lt_row(float* s, float scale_log2, int li
 // batched_row's product form from precomputed t (s[] = t, masked columns 0): A
 // into pk with Q = e^a carried right to left.  False if a group product reached
 // 2^64 (the caller redoes the row per element).
-__device__ __forceinline__ bool batched_from_t(const float* s, uint32_t* pk, float Q) {
+__device__ __forceinline__ bool batched_from_t(const float* s, uint32_t* pk, float Q,
+                                               float limit = kBatchedMax) {
+  const float q_in = Q;
   constexpr int NG = kBlock / 16;
   float P[NG];
 #pragma unroll
@@ -313,13 +371,14 @@ __device__ __forceinline__ bool batched_from_t(const float* s, uint32_t* pk, flo
     for (int g = 0; g < NG; ++g) P[g] = fmaf(P[g], s[16 * g + i], P[g]);
   bool ok = true;
 #pragma unroll
-  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < kBatchedMax);
+  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < limit);
   float F[NG];
 #pragma unroll
   for (int g = NG - 1; g >= 0; --g) {
     F[g] = Q * rcp(P[g]);
     Q = F[g];
   }
+  if (limit > kBatchedMax) ok = ok && batched_seed_ok(Q, q_in);  // the wider range
 #pragma unroll
   for (int i = 0; i < 16; i += 2)
 #pragma unroll

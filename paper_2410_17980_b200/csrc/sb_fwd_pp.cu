@@ -452,7 +452,9 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
         }
         if (kSkip && __any_sync(0xffffffffu, slow)) {
-          // a group product reached 2^64: per-element product form from t (a is exact)
+          // a group product reached 2^64: the wider batched range, else the
+          // per-element product form from t (a is exact either way)
+          if (slow) slow = !batched_from_t(s, pk, ex2(a2_in), kBatchedWide);
           if (slow) {
             float Ql = ex2(a2_in), an = 0.0f;
 #pragma unroll
@@ -470,6 +472,20 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           tmem_ld32(tS, s);
           tmem_ld32(tS + 32, s + 32);
           tmem_wait_ld();
+          if (slow) {  // the wider batched range (sb_common.cuh) first
+            float lsum = 0.0f;
+            const bool okw = diag ? batched_row_wide<true>(s, pk, sl2, lim, ex2(a2), lsum)
+                                  : batched_row_wide<false>(s, pk, sl2, kBlock, ex2(a2), lsum);
+            if (okw) {
+              a2 -= lsum;
+              slow = false;
+            }
+          }
+          if (__any_sync(0xffffffffu, slow)) {  // s[] holds t now: raw S again (warp-collective)
+            tmem_ld32(tS, s);
+            tmem_ld32(tS + 32, s + 32);
+            tmem_wait_ld();
+          }
           if (slow) {
             // per-element product form for A; the row's lt from each 16-column
             // group's product of r (one lg2 per group), or the exact softplus sum
