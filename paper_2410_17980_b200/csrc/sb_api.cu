@@ -100,12 +100,18 @@ sb::Geom geom(const sb_params_t* p) {
   g.sl = p->stride_l;
   g.cu = p->cu_seqlens;
   // grouped_order: units per group such that the group's K and V (bf16) fit a
-  // 32 MiB slice of the 126 MB L2, at least 8
+  // 16 MiB slice of the 126 MB L2 (at least 8 units; measured best for phase 2 at
+  // C2).  A small problem (fewer than ~4 forward items per SM: strong-scaling
+  // shares, short varlen batches) is one group in global longest-first order
+  // instead, so its heaviest items all start first.
   // (varlen: the mean sequence length, so a group holds about as many tokens)
   const int64_t len = (p->cu_seqlens && p->batch > 0) ? p->total_tokens / p->batch : p->seqlen;
   const int64_t unit_bytes = 4 * std::max<int64_t>(1, len) * p->head_dim;
   const int64_t bh = (int64_t)p->batch * p->heads;
-  g.ugroup = (int)std::max<int64_t>(1, std::min<int64_t>(bh, std::max<int64_t>(8, (32ll << 20) / unit_bytes)));
+  const int64_t fwd_items = (int64_t)((g.n_qt + 1) / 2) * bh;
+  int64_t ug = std::max<int64_t>(8, (16ll << 20) / unit_bytes);
+  if (fwd_items < 4 * 148) ug = bh;
+  g.ugroup = (int)std::max<int64_t>(1, std::min<int64_t>(bh, ug));
   return g;
 }
 
