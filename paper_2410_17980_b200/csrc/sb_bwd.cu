@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (!it.valid) continue;
         const Unit& u = it.u;
         if (ni >= 1) mbar_wait(bar_qdofree, (ni - 1) & 1);
+        SB_TR(args, 0, ni, 12);
         if (leader) {
           const int nw = it.has1 ? 2 : 1;
           mbar_expect_tx(bar_qdo, nw * 2 * C::kQBytes);
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       float Ma = Mrow[tile_of(it.kb_lo)];  // M of the next tile, loaded one tile ahead
       float bsum = 0.0f;                   // running b (blocked.py:342, :354)
+      if (tr) SB_TR(args, w, nwi, 11);
       for (int j = 0; j < n_w; ++j) {
         const int kb = it.kb_lo + j, gi = ig + j;
         const bool live = row_valid && kb >= my_first && kb <= my_qb;
@@ -575,6 +577,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // store mode: the last tile's TMA store must have read the buffer too
       if (kStoreZ) mbar_wait(zempty, (ig + n_w - 1) & 1);
       if (tr) SB_TR(args, w, 0, 15);
+      if (tr) SB_TR(args, w, nwi, 9);
       tc_fence_after();
       // dQ rows leave in 64-column halves through this warp's 4 KB slice of the
       // (now idle: `done`) dZ buffer as coalesced row segments
@@ -594,6 +597,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         warp_store_rows<8>(v, scale, stage, args.dq + u.out_off + (int64_t)row0 * g.sl + c * 64,
                            g.sl, nvalid);
       }
+      if (tr) SB_TR(args, w, nwi, 10);
       ig += n_w;
       ++nwi;
     }
