@@ -117,3 +117,24 @@ def test_varlen_host_offsets_same_results():
     torch.cuda.synchronize()
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("store", [False, True])
+def test_varlen_skip_backward_equals_per_sequence_runs(store):
+    """Skip on + packed varlen through forward AND the two-phase backward (both
+    backward modes): every sequence bit-identical to its uniform-batch run."""
+    import paper_2410_17980_b200 as sb
+    lens = [1024, 300, 640, 129]
+    H, d = 2, 128
+    (q, k, v, d_o), cu = packed(lens, H, d, seed=4)  # random logits: most tiles skip
+    o, log_rem, st, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu, skip=True, skip_eps=1e-6)
+    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, store_tiles=store)
+    torch.cuda.synchronize()
+    assert st.skipped > 0
+    for b, L in enumerate(lens):
+        qs, ks, vs, ds = (seq(t, cu, b) for t in (q, k, v, d_o))
+        o1, _, _, c1 = sb.blocked_forward(qs, ks, vs, skip=True, skip_eps=1e-6)
+        dq1, dk1, dv1, _ = sb.blocked_backward_twophase(c1, ds, store_tiles=store)
+        assert torch.equal(seq(o, cu, b), o1), b
+        for got, ref in ((dq, dq1), (dk, dk1), (dv, dv1)):
+            assert torch.equal(seq(got, cu, b), ref), b
