@@ -10,6 +10,10 @@
 //   tiles, b = N snapshot, dK += dZ^T Q, dV += A^T dO — owned rows, no atomics,
 //   deterministic.  dK and dV are accumulated in TMEM with M = 128 keys (A^T /
 //   dZ^T reach the tensor core through MN-major smem descriptors).
+// Store mode (default when the workspace fits): phase 1 also TMA-stores every dZ
+//   tile; phase 2 (sb_bwd_kvs_kernel) loads it instead of recomputing dO V^T and
+//   dZ, and recomputes only A (same results bit for bit: the stored tiles are the
+//   values the recompute-mode phase 2, sb_bwd_kv_kernel, would compute).
 //
 // Both phases use the ping-pong layout of sb_fwd_pp.cu: two stick warpgroups
 // per CTA (thread r <-> TMEM lane r <-> query row, all 64 key columns of a tile
@@ -20,7 +24,9 @@
 // prod_{c'>c} r_c', sigma = t/(1+t), r = 1/(1+t), with one rcp per 16 columns
 // (batched reciprocal, recompute_row).
 // Warps: 0-3 WG0, 4-7 WG1, 8 TMA producer (+TMEM allocator), 9/10 MMA for WG0/WG1,
-// 11 idle; warpgroup 2 hands its registers to the stick warpgroups (setmaxnreg).
+// 11 phase 1's V producer / phase 2's dO producer (store mode: 10 loads dZ, 9 is
+// the single issuer); warpgroup 2 hands its registers to the stick warpgroups
+// (setmaxnreg).
 #include "sb_args.cuh"
 
 namespace sb {

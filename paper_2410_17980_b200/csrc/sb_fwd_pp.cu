@@ -1,4 +1,5 @@
-// Stick-breaking attention forward, ping-pong variant (skip off), sm_100a.
+// Stick-breaking attention forward, persistent ping-pong kernel (skip off and,
+// with kSkip, skip on), sm_100a.
 //
 // Same algorithm as sb_fwd.cu (reference blocked.py:129-206, two_phase=True),
 // organised for throughput: a work item is TWO 128-row query tiles of the same
@@ -12,7 +13,9 @@
 // Per element (product form, sb_common.cuh): t = 2^Z, r = 1/(1+t), sigma = t*r,
 // A = sigma * (e^a * prod of r to the right), with one rcp per 16 columns
 // (batched_row).  The row total of lt for `a` is -lg2 of the tile's product of
-// (1+t) (exact softplus sum on the per-element slow path).
+// (1+t); rows outside the batched range retry a wider range, then take the
+// per-element path (sb_common.cuh).  kSkip computes exact lt sums for the skip
+// decisions (see the kernel's comment).
 //
 // Warps: 0-3 WG0, 4-7 WG1, 8 TMA producer (+TMEM allocator), 9 MMA for WG0,
 // 10 MMA for WG1.
