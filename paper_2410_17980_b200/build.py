@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False,
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(CSRC, src.replace(".cu", f"{tag}.o"))
+        # per-process object names and an atomic rename of the library: several ranks
+        # (torchrun) may find the library stale at once
+        obj = os.path.join(CSRC, src.replace(".cu", f"{tag}.{os.getpid()}.o"))
         cmd = [NVCC, *FLAGS, *extra, "-c", path, "-o", obj]
         jobs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                                 stderr=subprocess.STDOUT, text=True)))
@@ -68,13 +70,15 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False,
         if proc.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{out}")
         objs.append(obj)
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib, *objs,
+    tmp = f"{lib}.{os.getpid()}.tmp"
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     for o in objs:
         os.remove(o)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, lib)
     if verbose:
         print("\n".join(log))
     return lib
