@@ -183,10 +183,17 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; SB_BENCH_BACKEND=gloo lets a plumbing check run several ranks
+    # on one GPU (ranks then share device local % device_count)
+    backend = os.environ.get("SB_BENCH_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2410_17980_b200 as sb
     from paper_2410_17980_b200 import build as sbbuild
@@ -232,7 +239,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     clocks.start()
     time.sleep(0.3)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
