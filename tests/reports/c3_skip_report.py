@@ -1,6 +1,9 @@
 #!/usr/bin/env python3
 """C3 long-context block-skipping report (BASELINE.json configs[2]).
 
+A checker: it lives under tests/ because it runs the oracle to verify the GPU skip
+decisions (the oracle is test infrastructure only).
+
 B=1, H=32, L=32768, d=128 bf16, skip on (skip_eps = 1e-6, the reference's f32
 default for non-f64 inputs).  For each input family (random, logit shift mu=-6
 and mu=-8, saturating, dead) it reports:
@@ -11,7 +14,7 @@ and mu=-8, saturating, dead) it reports:
     in float64 on the same bf16-rounded inputs (families where the oracle is cheap).
 Prints one JSON object; `--out` also writes it to a file.
 
-    python tools/skip_report.py [--L 32768] [--H 32] [--check-heads 1] [--out f.json]
+    python tests/reports/c3_skip_report.py [--L 32768] [--H 32] [--check-heads 1] [--out f.json]
 """
 
 from __future__ import annotations
@@ -25,7 +28,7 @@ import time
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402  (checker only)

@@ -1,6 +1,9 @@
 #!/usr/bin/env python3
 """Parity / bench harness writing the reference CLI's artifacts.
 
+A checker (it runs the oracle for `equiv`), so it lives under tests/ with the other
+test infrastructure.
+
 `equiv` and `bench` produce `equiv.csv`, `bench.csv` and `manifest.json` with the column
 schemas of the reference's `sb equiv` / `sb bench` (cli.py:343-344, :453-455, :128-152), so
 results line up with the reference's tooling, but measure this package's CUDA path:
@@ -19,8 +22,8 @@ results line up with the reference's tooling, but measure this package's CUDA pa
 
 Only d_block = 64 exists on the GPU path (blocked.py:41 DEFAULT_BLOCK); head_dim 64 or 128.
 
-    python tools/harness.py equiv [--lengths 1,7,64,100,256,512] [--d 64] [--out DIR]
-    python tools/harness.py bench [--lengths 256,1024,4096] [--d 64] [--input random] [--out DIR]
+    python tests/reports/reference_harness.py equiv [--lengths 1,7,64,100,256,512] [--d 64] [--out DIR]
+    python tests/reports/reference_harness.py bench [--lengths 256,1024,4096] [--d 64] [--input random] [--out DIR]
 """
 
 from __future__ import annotations
@@ -37,7 +40,7 @@ import sys
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402  (checker only)

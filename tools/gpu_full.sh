@@ -4,7 +4,7 @@ timeout 300 python -m pytest tests -x -q -m gpu 2>&1 | tail -25 > gpurun_out/pyt
 timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 400 python bench.py > gpurun_out/bench.log 2>&1
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1
-timeout 600 python tools/skip_report.py --out gpurun_out/c3_skip.json > gpurun_out/skip.log 2>&1
+timeout 600 python tests/reports/c3_skip_report.py --out gpurun_out/c3_skip.json > gpurun_out/skip.log 2>&1
 for n in 2 4 8; do timeout 200 python tools/varlen_bench.py --simulate-ranks $n; done > gpurun_out/c4.log 2>&1
 bash tools/gpu_ncu.sh
 tail -n 2 gpurun_out/bench.log gpurun_out/bench_ref.log gpurun_out/skip.log gpurun_out/smoke.log gpurun_out/pytest_gpu.log
