@@ -690,6 +690,7 @@ struct LiveQt {
 // striding (round k: CTA c takes item k*G + c, or k*G + G-1-c on odd rounds, so
 // heavy-first rounds alternate direction: max/mean CTA load 1.05 vs 1.07).
 constexpr bool kDynamicKV = false;
+constexpr bool kDynamicKVS = true;  // store-mode phase 2 (static snake: 4% CTA imbalance at C2)
 __device__ __forceinline__ int snake_item(int k) {
   return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
 }
@@ -1204,7 +1205,7 @@ struct BwdKVSCfg {
   static constexpr int kOffA = kOffDO + kQBytes;            // key block 0 then 1
   static constexpr int kOffZ = kOffA + 2 * kPBytes;         // dZ ring: 2 x (block 0, block 1)
   static constexpr int kOffBar = kOffZ + 2 * 2 * kPBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 4 + 9;
+  static constexpr int kNumBars = 1 + 2 * kStages + 2 + 4 + 9 + 8;  // + work-queue ring
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
@@ -1241,8 +1242,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* kv_free = sfull + 7;
   uint64_t* acc_free = sfull + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
+  // dynamic work queue (kDynamicKVS): warp 8 takes items from a global counter (the
+  // N header's second word) and hands them to every other role through this ring
+  const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), acc_free + 1, acc_free + 5};
+  auto next_item = [&](int kq) -> int {
+    if (!kDynamicKVS) {
+      const int idx = snake_item(kq);
+      return idx < n_items ? idx : -1;
+    }
+    return warp == 8 ? sched_produce(sq, kq, args.sched + 1, n_items) : sched_consume(sq, kq);
+  };
 
   if (threadIdx.x == 0) {
+    if (kDynamicKVS) sched_init(sq, 11);  // consumers: sticks 0-7, warps 9, 10, 11
     mbar_init(bar_kv, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_qfull + s, 1);
@@ -1288,7 +1300,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       // L2 look-ahead (see KVCursor): this warp's stream only
       KVCursor ahead{&g, args.first_kb, n_items, -1, 0};
-      bool more = ahead.open_next_item();
+      bool more = !kDynamicKVS && ahead.open_next_item();  // look-ahead needs a static order
       auto prefetch_one = [&]() {
         if (!more) return;
         if (leader) {
@@ -1308,8 +1320,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int i = 0; i < kPrefetch; ++i) prefetch_one();
       int jg = 0, ni = 0;
       for (int kq = 0;; ++kq) {
-        const int idx = snake_item(kq);
-        if (idx >= n_items) break;
+        const int idx = next_item(kq);
+        if (idx < 0) break;
         const KVItem wi = kv_item(g, idx);
         if (!wi.valid) continue;
         const Unit& u = wi.u;
@@ -1404,8 +1416,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       int jg = 0, ni = 0;
       for (int kq = 0;; ++kq) {
-        const int idx = snake_item(kq);
-        if (idx >= n_items) break;
+        const int idx = next_item(kq);
+        if (idx < 0) break;
         const KVItem wi = kv_item(g, idx);
         if (!wi.valid) continue;
         const Unit& u = wi.u;
@@ -1467,8 +1479,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (tr) SB_TR(args, w, 0, 14);
     int jg = 0, ni = 0;
     for (int kq = 0;; ++kq) {
-      const int idx = snake_item(kq);
-      if (idx >= n_items) break;
+      const int idx = next_item(kq);
+      if (idx < 0) break;
       const KVItem wi = kv_item(g, idx);
       if (!wi.valid) continue;
       const Unit& u = wi.u;
@@ -1619,6 +1631,8 @@ static int launch_bwd(const CUtensorMap& tq, const CUtensorMap& tdo, const CUten
       auto kern = sb_bwd_kvs_kernel<D>;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
       if (e != cudaSuccess) return (int)e;
+      if (kDynamicKVS && (e = cudaMemsetAsync(a.sched + 1, 0, sizeof(unsigned), stream)) != cudaSuccess)
+        return (int)e;
       kern<<<grid, kBwdThreads, C::kSmem, stream>>>(tq, tdo, tk, tz, a);
     } else {
       using C = BwdKVCfg<D>;
