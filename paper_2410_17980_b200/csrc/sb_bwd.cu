@@ -63,43 +63,63 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
   for (int c = 0; c < kBlock; ++c) { s[c] *= E; sg[c] = E; }
   return;
 #endif
+  // The multiplies run as packed f32x2 (FMUL2 / FFMA2, sb_common.cuh batched_row):
+  // the scale on adjacent column pairs, everything else on the group pairs
+  // (0,1) and (2,3), i.e. columns (c, c+16); bit-identical to the scalar form.
   constexpr int NG = kBlock / 16;
-  float tot[NG];
+  const float2 sl2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
-  for (int g = 0; g < NG; ++g) tot[g] = 1.0f;
+  for (int c = 0; c < kBlock; c += 2) {
+    const float2 z = mul2(make_float2(s[c], s[c + 1]), sl2);
+    float t0 = ex2(z.x), t1 = ex2(z.y);
+    if (kDiag) {
+      t0 = c < lim ? t0 : 0.0f;
+      t1 = c + 1 < lim ? t1 : 0.0f;
+    }
+    s[c] = t0;
+    s[c + 1] = t1;
+  }
+  float2 tp[2] = {make_float2(1.0f, 1.0f), make_float2(1.0f, 1.0f)};
 #pragma unroll
   for (int i = 0; i < 16; ++i)
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int c = 16 * g + i;
-      float tt = ex2(s[c] * scale_log2);
-      if (kDiag) tt = c < lim ? tt : 0.0f;
-      s[c] = tt;
-      tot[g] = fmaf(tot[g], tt, tot[g]);
-      sg[c] = tot[g];
+    for (int h = 0; h < 2; ++h) {
+      const int c = 32 * h + i;
+      tp[h] = fma2(tp[h], make_float2(s[c], s[c + 16]), tp[h]);
+      sg[c] = tp[h].x;
+      sg[c + 16] = tp[h].y;
     }
+  const float tot[NG] = {tp[0].x, tp[0].y, tp[1].x, tp[1].y};
   bool ok = true;
 #pragma unroll
   for (int g = 0; g < NG; ++g) ok = ok && (tot[g] < kBatchedMax);
   auto fast = [&]() {
-    float inv[NG], K[NG];
+    float2 inv[2], K[2];
     float Q = E;
-#pragma unroll
-    for (int g = NG - 1; g >= 0; --g) {
-      inv[g] = rcp(tot[g]);
-      K[g] = Q * inv[g];
-      Q = K[g];
-    }
+    inv[1].y = rcp(tot[3]);
+    K[1].y = Q * inv[1].y;
+    inv[1].x = rcp(tot[2]);
+    K[1].x = K[1].y * inv[1].x;
+    inv[0].y = rcp(tot[1]);
+    K[0].y = K[1].x * inv[0].y;
+    inv[0].x = rcp(tot[0]);
+    K[0].x = K[0].y * inv[0].x;
 #pragma unroll
     for (int i = 15; i >= 0; --i)
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        const int c = 16 * g + i;
-        const float t = s[c];
-        const float u = i ? t * sg[c - 1] : t;
-        if (kSigma) sg[c] = u * inv[g];
-        s[c] = u * K[g];
-        if (kSigma) inv[g] = fmaf(inv[g], t, inv[g]);
+      for (int h = 0; h < 2; ++h) {
+        const int c = 32 * h + i;
+        const float2 t = make_float2(s[c], s[c + 16]);
+        const float2 u = i ? mul2(t, make_float2(sg[c - 1], sg[c + 15])) : t;
+        if (kSigma) {
+          const float2 sgm = mul2(u, inv[h]);
+          sg[c] = sgm.x;
+          sg[c + 16] = sgm.y;
+        }
+        const float2 a = mul2(u, K[h]);
+        s[c] = a.x;
+        s[c + 16] = a.y;
+        if (kSigma) inv[h] = fma2(inv[h], t, inv[h]);
       }
   };
   if (ok) {
@@ -1107,16 +1127,26 @@ __device__ __forceinline__ bool recompute_a_pipe(float* s, uint32_t* pk, float s
   for (int c = 0; c < kBlock; c += 2) pk[c >> 1] = pack_bf16(s[c] * E, s[c + 1] * E);
   return true;
 #endif
+  // packed f32x2 multiplies on adjacent column pairs (FMUL2; the product chain
+  // stays scalar): same operations per element, bit-identical
+  const float2 sl2 = make_float2(scale_log2, scale_log2);
   float P[64];
   float tot = 1.0f;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {  // prologue: pass 1 of group 3
+  for (int i = 0; i < 16; i += 2) {  // prologue: pass 1 of group 3
     const int c = 48 + i;
-    float tt = ex2(s[c] * scale_log2);
-    if (kDiag) tt = c < lim ? tt : 0.0f;
-    s[c] = tt;
-    tot = fmaf(tot, tt, tot);
+    const float2 z = mul2(make_float2(s[c], s[c + 1]), sl2);
+    float t0 = ex2(z.x), t1 = ex2(z.y);
+    if (kDiag) {
+      t0 = c < lim ? t0 : 0.0f;
+      t1 = c + 1 < lim ? t1 : 0.0f;
+    }
+    s[c] = t0;
+    s[c + 1] = t1;
+    tot = fmaf(tot, t0, tot);
     P[c] = tot;
+    tot = fmaf(tot, t1, tot);
+    P[c + 1] = tot;
   }
   bool ok = tot < kBatchedMax;
   float Kn = E * rcp(tot);  // K of the group whose product pass runs next
@@ -1124,32 +1154,39 @@ __device__ __forceinline__ bool recompute_a_pipe(float* s, uint32_t* pk, float s
 #pragma unroll
   for (int g = 2; g >= 0; --g) {
     tot = 1.0f;
-    float a0 = 0.0f;
+    const float2 K2 = make_float2(Kn, Kn);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int c = 16 * g + i;  // pass 1, group g
-      float tt = ex2(s[c] * scale_log2);
-      if (kDiag) tt = c < lim ? tt : 0.0f;
-      s[c] = tt;
-      tot = fmaf(tot, tt, tot);
+    for (int i = 0; i < 16; i += 2) {
+      const int c = 16 * g + i;  // pass 1, group g (two columns)
+      const float2 z = mul2(make_float2(s[c], s[c + 1]), sl2);
+      float t0 = ex2(z.x), t1 = ex2(z.y);
+      if (kDiag) {
+        t0 = c < lim ? t0 : 0.0f;
+        t1 = c + 1 < lim ? t1 : 0.0f;
+      }
+      s[c] = t0;
+      s[c + 1] = t1;
+      tot = fmaf(tot, t0, tot);
       P[c] = tot;
-      const int c2 = c + 16;  // pass 2, group g + 1
-      const float u = i ? s[c2] * P[c2 - 1] : s[c2];
-      const float a = u * Kn;
-      if (i & 1) pk[c2 >> 1] = pack_bf16(a0, a);
-      else a0 = a;
+      tot = fmaf(tot, t1, tot);
+      P[c + 1] = tot;
+      const int c2 = c + 16;  // pass 2, group g + 1 (two columns)
+      const float2 t2 = make_float2(s[c2], s[c2 + 1]);
+      const float2 u = i ? mul2(t2, make_float2(P[c2 - 1], P[c2])) : make_float2(t2.x, t2.y * P[c2]);
+      const float2 a = mul2(u, K2);
+      pk[c2 >> 1] = pack_bf16(a.x, a.y);
     }
     ok = ok && (tot < kBatchedMax);
     Kn = Q * rcp(tot);
     Q = Kn;
   }
-  float a0 = 0.0f;
+  const float2 K2 = make_float2(Kn, Kn);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {  // epilogue: pass 2 of group 0
-    const float u = i ? s[i] * P[i - 1] : s[i];
-    const float a = u * Kn;
-    if (i & 1) pk[i >> 1] = pack_bf16(a0, a);
-    else a0 = a;
+  for (int i = 0; i < 16; i += 2) {  // epilogue: pass 2 of group 0
+    const float2 t2 = make_float2(s[i], s[i + 1]);
+    const float2 u = i ? mul2(t2, make_float2(P[i - 1], P[i])) : make_float2(t2.x, t2.y * P[i]);
+    const float2 a = mul2(u, K2);
+    pk[i >> 1] = pack_bf16(a.x, a.y);
   }
   return ok;
 }

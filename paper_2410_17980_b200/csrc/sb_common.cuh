@@ -234,6 +234,25 @@ __device__ __forceinline__ bool batched_seed_ok(float seed_min, float q_in) {
   return seed_min >= kSeedMin || q_in < kMassNeg;
 }
 
+// f32x2 step of pass 2 on the group pair (g, g+1) = columns (c, c+16), (c+1, c+17):
+// A_i = t_i * F, F *= (1 + t_i) for two columns of both groups.
+__device__ __forceinline__ float2 x2_pass2_step(const float* s, uint32_t* pk, int c, float2 F) {
+  const float2 t0 = make_float2(s[c], s[c + 16]);
+  const float2 t1 = make_float2(s[c + 1], s[c + 17]);
+  const float2 a0 = mul2(t0, F);
+  F = fma2(F, t0, F);
+  const float2 a1 = mul2(t1, F);
+  F = fma2(F, t1, F);
+  pk[c >> 1] = pack_bf16(a0.x, a1.x);
+  pk[(c + 16) >> 1] = pack_bf16(a0.y, a1.y);
+  return F;
+}
+
+// The multiplies run as packed f32x2 (FMUL2 / FFMA2: two lanes per FMA-pipe
+// instruction, each rounded exactly like the scalar op, so the results are the
+// scalar form's bit for bit): the scale on adjacent column pairs, the product and
+// seed chains on the group pairs (0,1) and (2,3).  That halves the FMA-pipe work,
+// which otherwise matches the MUFU's (tools/ubench/ub_rowmath.cu).
 template <bool kDiag>
 __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_log2, int lim,
                                             float& Q, float& Dhi, float& Dlo) {
@@ -243,46 +262,40 @@ __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_
   Dhi = Dlo = 1.0f;
   return true;
 #endif
-  // pass 1: t into s[] and the group products, four independent chains
-  constexpr int NG = kBlock / 16;
-  float P[NG];
+  // pass 1: t into s[], then the group products (two f32x2 chains of group pairs)
+  const float2 sl2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
-  for (int g = 0; g < NG; ++g) P[g] = 1.0f;
+  for (int c = 0; c < kBlock; c += 2) {
+    const float2 z = mul2(make_float2(s[c], s[c + 1]), sl2);
+    float t0 = ex2(z.x), t1 = ex2(z.y);  // t = inf makes P = inf: slow path
+    if (kDiag) {
+      t0 = c < lim ? t0 : 0.0f;
+      t1 = c + 1 < lim ? t1 : 0.0f;
+    }
+    s[c] = t0;
+    s[c + 1] = t1;
+  }
+  float2 P[2] = {make_float2(1.0f, 1.0f), make_float2(1.0f, 1.0f)};
 #pragma unroll
   for (int i = 0; i < 16; ++i)
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int c = 16 * g + i;
-      float tt = ex2(s[c] * scale_log2);  // t = inf makes P = inf: slow path
-      if (kDiag) tt = c < lim ? tt : 0.0f;
-      s[c] = tt;
-      P[g] = fmaf(P[g], tt, P[g]);
-    }
-  bool ok = true;
-#pragma unroll
-  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < kBatchedMax);
+    for (int h = 0; h < 2; ++h) P[h] = fma2(P[h], make_float2(s[32 * h + i], s[32 * h + 16 + i]), P[h]);
   // group seeds F_g = Q_g / P_g, right to left
-  float F[NG];
-#pragma unroll
-  for (int g = NG - 1; g >= 0; --g) {
-    F[g] = Q * rcp(P[g]);
-    Q = F[g];
-  }
-  // pass 2: A_i = t_i * F, F *= (1 + t_i), four independent chains
+  float2 F[2];
+  F[1].y = Q * rcp(P[1].y);
+  F[1].x = F[1].y * rcp(P[1].x);
+  F[0].y = F[1].x * rcp(P[0].y);
+  F[0].x = F[0].y * rcp(P[0].x);
+  Q = F[0].x;
+  // pass 2: A_i = t_i * F, F *= (1 + t_i)
 #pragma unroll
   for (int i = 0; i < 16; i += 2)
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int c = 16 * g + i;
-      const float a0 = s[c] * F[g];
-      F[g] = fmaf(F[g], s[c], F[g]);
-      const float a1 = s[c + 1] * F[g];
-      F[g] = fmaf(F[g], s[c + 1], F[g]);
-      pk[c >> 1] = pack_bf16(a0, a1);
-    }
-  Dhi = P[3] * P[2];
-  Dlo = P[1] * P[0];
-  return ok;
+    for (int h = 0; h < 2; ++h) F[h] = x2_pass2_step(s, pk, 32 * h + i, F[h]);
+  Dhi = P[1].y * P[1].x;
+  Dlo = P[0].y * P[0].x;
+  return P[0].x < kBatchedMax && P[0].y < kBatchedMax && P[1].x < kBatchedMax &&
+         P[1].y < kBatchedMax;
 }
 
 // batched_row in the wider range (slow branch of the skip-off forward): s[] = raw S
