@@ -41,7 +41,7 @@ static_assert(128 * kRegsLowKV + 256 * kRegsHighKV <= kBwdThreads * kRegsLaunch,
 static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "register budget");
 
 // Recompute of one row of a tile: on entry s[] = raw q.k dot products, on exit
-// s[c] = A_c and sg[c] = sigma_c (both 0 where masked).  E = e^M (the M
+// s[c] = A_c and sg[c] = -sigma_c (both 0 where masked; negated for dz_row).  E = e^M (the M
 // snapshot in linear space).
 // Batched reciprocal per group of 16 columns (see batched_row in sb_common.cuh):
 // with P_i = prod_{k<=i} (1+t_k) (within the group), u_i = t_i P_{i-1} and one
@@ -94,6 +94,7 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
 #pragma unroll
   for (int g = 0; g < NG; ++g) ok = ok && (tot[g] < kBatchedMax);
   auto fast = [&]() {
+    // ninv = -1/P_i (running): sg leaves as -sigma for dz_row's FFMA2
     float2 inv[2], K[2];
     float Q = E;
     inv[1].y = rcp(tot[3]);
@@ -104,6 +105,8 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
     K[0].y = K[1].x * inv[0].y;
     inv[0].x = rcp(tot[0]);
     K[0].x = K[0].y * inv[0].x;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) inv[h] = make_float2(-inv[h].x, -inv[h].y);
 #pragma unroll
     for (int i = 15; i >= 0; --i)
 #pragma unroll
@@ -143,7 +146,7 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
         const float r = rcp(1.0f + t);
         const float sgm = fminf(t * r, 1.0f);  // t = inf: NaN -> 1
         s[c] = sgm * Q;
-        sg[c] = sgm;
+        sg[c] = -sgm;
         Q *= r;
       }
     }
@@ -164,28 +167,39 @@ __device__ __forceinline__ void load_dat(float* s, uint32_t taddr, float off) {
 }
 
 // dZ = dAt - sigma*(prefix(dAt) + b), packed to bf16; returns b + rowsum(dAt).
-// Two independent prefix chains (column halves); the right half's offset
-// b + sum(left half) is applied afterwards with one FFMA per element.
-__device__ __forceinline__ float dz_row(const float* dat, const float* sg, float b, uint32_t* pk) {
-  constexpr int H = kBlock / 2;
-  float xl = b, xr = 0.0f;
-  float zr[H];
+// nsg[] = -sigma (recompute_row's output).  Four prefix chains of 16 columns run
+// as two f32x2 pairs, chains (0,1) and (2,3) = columns (c, c+16): a first pass
+// sums each chain, the second runs every chain from its exact offset
+// (b + the sums to its left) with one FADD2 and one FFMA2 per column pair.
+__device__ __forceinline__ float dz_row(const float* dat, const float* nsg, float b, uint32_t* pk) {
+  float2 sa = make_float2(0.0f, 0.0f), sb2 = sa;
 #pragma unroll
-  for (int c = 0; c < H; c += 2) {
-    xl += dat[c];
-    xr += dat[H + c];
-    const float z0 = fmaf(-sg[c], xl, dat[c]);
-    zr[c] = fmaf(-sg[H + c], xr, dat[H + c]);
-    xl += dat[c + 1];
-    xr += dat[H + c + 1];
-    const float z1 = fmaf(-sg[c + 1], xl, dat[c + 1]);
-    zr[c + 1] = fmaf(-sg[H + c + 1], xr, dat[H + c + 1]);
-    pk[c >> 1] = pack_bf16(z0, z1);
+  for (int c = 0; c < 16; ++c) {
+    sa = add2(sa, make_float2(dat[c], dat[c + 16]));
+    sb2 = add2(sb2, make_float2(dat[c + 32], dat[c + 48]));
   }
+  const float o1 = b + sa.x, o2 = o1 + sa.y, o3 = o2 + sb2.x;
+  float2 xa = make_float2(b, o1), xb = make_float2(o2, o3);
+  float2 za0 = xa, zb0 = xb;
 #pragma unroll
-  for (int c = 0; c < H; c += 2)
-    pk[(H + c) >> 1] = pack_bf16(fmaf(-sg[H + c], xl, zr[c]), fmaf(-sg[H + c + 1], xl, zr[c + 1]));
-  return xl + xr;
+  for (int c = 0; c < 16; ++c) {
+    const float2 da = make_float2(dat[c], dat[c + 16]);
+    const float2 db = make_float2(dat[c + 32], dat[c + 48]);
+    xa = add2(xa, da);
+    xb = add2(xb, db);
+    const float2 za = fma2(make_float2(nsg[c], nsg[c + 16]), xa, da);
+    const float2 zb = fma2(make_float2(nsg[c + 32], nsg[c + 48]), xb, db);
+    if (c & 1) {
+      pk[c >> 1] = pack_bf16(za0.x, za.x);
+      pk[(c + 16) >> 1] = pack_bf16(za0.y, za.y);
+      pk[(c + 32) >> 1] = pack_bf16(zb0.x, zb.x);
+      pk[(c + 48) >> 1] = pack_bf16(zb0.y, zb.y);
+    } else {
+      za0 = za;
+      zb0 = zb;
+    }
+  }
+  return o3 + sb2.y;
 }
 
 __device__ __forceinline__ void store_row_sw128(uint32_t row_addr, int r, const uint32_t* pk) {

@@ -336,6 +336,11 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(b64_of(a)), "l"(b64_of(b)), "l"(b64_of(c)));
   return f2_of(d);
 }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(b64_of(a)), "l"(b64_of(b)));
+  return f2_of(d);
+}
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
   uint64_t d;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(b64_of(a)), "l"(b64_of(b)));
