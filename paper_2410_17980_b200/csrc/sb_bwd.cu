@@ -31,7 +31,8 @@
 
 namespace sb {
 
-constexpr int kBwdThreads = 12 * 32;  // WG0, WG1 stick; WG2 = producer, MMA0, MMA1, idle
+constexpr int kBwdThreads = 12 * 32;
+constexpr bool kPingPongQ = true;  // phase 1: the warpgroups take turns at the recompute  // WG0, WG1 stick; WG2 = producer, MMA0, MMA1, idle
 // setmaxnreg only redistributes the CTA's launch allocation (384 threads x 168
 // registers): 128 x low + 256 x high <= 384 x 168, otherwise .inc blocks forever.
 constexpr int kRegsLaunch = 168;
@@ -548,12 +549,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float scale = g.scale_log2 * kLn2;
     const bool tr = quarter == 0 && lane == 0;
     if (tr) SB_TR(args, w, 0, 14);
+    // Ping-pong of the MUFU-heavy recompute: the two warpgroups take turns (named
+    // barriers 1 and 2, FA3-style), so one's recompute overlaps the other's dW
+    // wait, dZ math and stores instead of both contending for the MUFU at once.
+    // Round k of an item: WG0 waits bar 1, recomputes, arrives on bar 2; WG1
+    // waits bar 2, recomputes, arrives on bar 1.  Both run max(n0, n1) rounds per
+    // item (a warpgroup without a tile in a round passes straight through).
+    const uint32_t bar_mine = 1 + w, bar_other = 2 - w;
+    auto pp_round_pass = [&]() {
+      named_bar_sync(bar_mine, 256);
+      named_bar_arrive(bar_other, 256);
+    };
+    if (kPingPongQ && w == 1) named_bar_arrive(1, 256);  // WG0 goes first
     int ig = 0, nwi = 0;
     for (int kq = 0;; ++kq) {
       const int idx = sched_consume(sq, kq);
       if (idx < 0) break;
       const QItem it = q_item(g, args.first_kb, idx, kStoreZ);
-      if (!it.valid || (w == 1 && !it.has1)) continue;
+      if (!it.valid) continue;
+      const int n0 = it.kbhi0 - it.kb_lo + 1, n1 = it.has1 ? it.kbhi1 - it.kb_lo + 1 : 0;
+      const int n_rounds = max(n0, n1);
+      if (w == 1 && !it.has1) {
+        if (kPingPongQ)
+          for (int j = 0; j < n_rounds; ++j) pp_round_pass();
+        continue;
+      }
       const Unit& u = it.u;
       const int qt = 2 * it.p + w;
       const int my_qb = 2 * qt + (r >> 6);
@@ -590,9 +610,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_arrive(sempty);  // S(j+1) may overwrite the buffer now
         if (tr) SB_TR(args, w, gi, 1);
         const bool diag = kb == my_qb;  // warp-uniform
+        if (kPingPongQ) named_bar_sync(bar_mine, 256);
         // dead rows/tiles run the same code with e^M = 0 and b = 0: A = 0, dZ = 0
         if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
         else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
+        if (kPingPongQ) named_bar_arrive(bar_other, 256);
         if (tr) SB_TR(args, w, gi, 2);
         mbar_wait(wfull, gi & 1);
         tc_fence_after();
@@ -613,6 +635,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_arrive(zfull);
         if (tr) SB_TR(args, w, gi, 6);
       }
+      if (kPingPongQ)
+        for (int j = n_w; j < n_rounds; ++j) pp_round_pass();
       mbar_wait(done, nwi & 1);
       // store mode: the last tile's TMA store must have read the buffer too
       if (kStoreZ) mbar_wait(zempty, (ig + n_w - 1) & 1);
@@ -642,6 +666,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ++nwi;
     }
   }
+  // ping-pong: WG1's last arrival on bar 1 still waits for WG0
+  if (kPingPongQ && warp < 4) named_bar_sync(1, 256);
   tc_fence_before();
   __syncthreads();
   if (warp == 8) tmem_dealloc<C::kTmemCols>(tbase);
