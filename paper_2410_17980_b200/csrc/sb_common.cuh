@@ -343,25 +343,49 @@ __device__ __forceinline__ bool batched_row_wide(float* s, uint32_t* pk, float s
   return true;
 }
 
+// softplus2 on two lanes (FFMA2 / FMUL2 / FADD2): per lane exactly softplus2's
+// operations, so the skip decisions built on it stay bit-exact.
+__device__ __forceinline__ float2 softplus2_x2(float2 Z, float2 t) {
+  const auto f2 = [](float v) { return make_float2(v, v); };
+  float2 p = fma2(t, f2(-1.0f / 6.0f), f2(1.0f / 5.0f));
+  p = fma2(p, t, f2(-1.0f / 4.0f));
+  p = fma2(p, t, f2(1.0f / 3.0f));
+  p = fma2(p, t, f2(-1.0f / 2.0f));
+  p = fma2(p, t, f2(1.0f));
+  const float2 small = mul2(p, mul2(t, f2(kLog2e)));
+  const float2 onep = add2(f2(1.0f), t);
+  float2 sp;
+  sp.x = t.x < 0.0625f ? small.x : lg2(onep.x);
+  sp.y = t.y < 0.0625f ? small.y : lg2(onep.y);
+  sp.x = Z.x > kSoftplusThr2 ? Z.x : sp.x;
+  sp.y = Z.y > kSoftplusThr2 ? Z.y : sp.y;
+  return sp;
+}
+
 // Skip-on forward (sb_fwd_pp_kernel<D, true>): the row's exact sum of lt for the
 // skip decisions, with the exact-path kernel's arithmetic (log_pass + the group
 // totals added 0..3: per 16-column group, right to left, f32), and t = 2^Z left
 // in s[] for the product form (0 where masked).  Returns the sum in log2 units.
+// The elementwise part runs on adjacent column pairs as f32x2; the sums keep
+// their order.
 template <bool kDiag>
 __device__ __forceinline__ float exact_lt_row(float* s, float scale_log2, int lim) {
+  const float2 sl2 = make_float2(scale_log2, scale_log2);
   float tot = 0.0f;
 #pragma unroll
   for (int g = 0; g < kBlock / 16; ++g) {
     float cum = 0.0f;
 #pragma unroll
-    for (int c = 15; c >= 0; --c) {
+    for (int c = 14; c >= 0; c -= 2) {
       const int col = 16 * g + c;
-      const float Z = s[col] * scale_log2;
-      const float t = ex2(Z);
-      const float sp = softplus2(Z, t);
-      const bool m = !kDiag || col < lim;
-      cum -= m ? sp : 0.0f;
-      s[col] = m ? t : 0.0f;
+      const float2 Z = mul2(make_float2(s[col], s[col + 1]), sl2);
+      const float2 t = make_float2(ex2(Z.x), ex2(Z.y));
+      const float2 sp = softplus2_x2(Z, t);
+      const bool m0 = !kDiag || col < lim, m1 = !kDiag || col + 1 < lim;
+      cum -= m1 ? sp.y : 0.0f;
+      cum -= m0 ? sp.x : 0.0f;
+      s[col] = m0 ? t.x : 0.0f;
+      s[col + 1] = m1 ? t.y : 0.0f;
     }
     tot += cum;
   }
@@ -370,7 +394,8 @@ __device__ __forceinline__ float exact_lt_row(float* s, float scale_log2, int li
 
 // batched_row's product form from precomputed t (s[] = t, masked columns 0): A
 // into pk with Q = e^a carried right to left.  False if a group product reached
-// 2^64 (the caller redoes the row per element).
+// 2^64 (the caller redoes the row per element).  Scalar: the f32x2 form spills in
+// the skip-on kernel.
 __device__ __forceinline__ bool batched_from_t(const float* s, uint32_t* pk, float Q,
                                                float limit = kBatchedMax) {
   const float q_in = Q;

@@ -9,7 +9,7 @@ profiles/<tag>_sass/<kernel>.txt with
   - the stick-math excerpt (the densest window of MUFU.EX2).
 and a summary table profiles/<tag>_sass/README.md.
 
-    python tools/sass_report.py [--lib paper_2410_17980_b200/libsbattn.so] [--tag r1_v6]
+    python tools/sass_report.py [--lib paper_2410_17980_b200/libsbattn.so] [--tag r1_v8]
 """
 
 from __future__ import annotations
@@ -22,7 +22,7 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CLASSES = ["UTCHMMA", "UTCBAR", "UTMALDG", "UTMASTG", "UTMAPF", "UTMACMDFLUSH", "LDTM", "STTM",
-           "MUFU.EX2", "MUFU.RCP", "MUFU.LG2", "FFMA", "FMUL", "FADD", "F2FP", "STS", "LDS", "STG",
+           "MUFU.EX2", "MUFU.RCP", "MUFU.LG2", "FFMA2", "FMUL2", "FADD2", "FFMA", "FMUL", "FADD", "F2FP", "STS", "LDS", "STG",
            "LDG", "SYNCS", "BAR", "SHFL"]
 
 
@@ -67,7 +67,7 @@ def demangle(name: str) -> str:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lib", default=os.path.join(ROOT, "paper_2410_17980_b200", "libsbattn.so"))
-    ap.add_argument("--tag", default="r1_v6")
+    ap.add_argument("--tag", default="r1_v8")
     a = ap.parse_args()
     sass = subprocess.run(["cuobjdump", "-sass", a.lib], capture_output=True, text=True,
                           check=True).stdout
@@ -108,13 +108,14 @@ def main():
     with open(os.path.join(out_dir, "README.md"), "w") as f:
         f.write(f"# SASS of libsbattn.so (sm_100a), `tools/sass_report.py --tag {a.tag}`\n\n")
         cols = ["UTCHMMA", "UTCBAR", "UTMALDG", "UTMASTG", "UTMAPF", "LDTM", "STTM", "MUFU.EX2",
-                "MUFU.RCP", "MUFU.LG2"]
+                "MUFU.RCP", "MUFU.LG2", "FFMA2", "FMUL2", "FADD2", "FFMA", "FMUL"]
         f.write("| kernel | instrs | " + " | ".join(cols) + " |\n")
         f.write("|---|---|" + "---|" * len(cols) + "\n")
         for short, n, h in rows:
             f.write(f"| {short} | {n} | " + " | ".join(str(h[c]) for c in cols) + " |\n")
         f.write("\nUTCHMMA = tcgen05.mma, UTCBAR = tcgen05.commit, UTMALDG/UTMASTG/UTMAPF = TMA "
-                "load/store/prefetch, LDTM/STTM = tcgen05.ld/st (TMEM).  Per-kernel files hold "
+                "load/store/prefetch, LDTM/STTM = tcgen05.ld/st (TMEM), FFMA2/FMUL2/FADD2 = packed "
+                "f32x2 arithmetic (two lanes per FMA-pipe instruction).  Per-kernel files hold "
                 "the MMA-issue and stick-math excerpts.\n")
     print(open(os.path.join(out_dir, "README.md")).read())
 
