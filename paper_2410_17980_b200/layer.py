@@ -43,19 +43,30 @@ def _attention(q, k, v, return_rem):
 
 
 class StickBreakingAttention(nn.Module):
+    """n_kv_head < n_head: grouped-query attention (the paper's 1.2B variant uses 12
+    query heads over 4 key/value heads; the reference toy
+    model has none): wk / wv project to n_kv_head heads and query head h reads
+    key/value head h // (n_head / n_kv_head).  The op sees the expanded heads, so
+    autograd sums each key/value head's gradient over its group."""
+
     def __init__(self, d_model: int, n_head: int, variant: str = "sb", group_norm: bool = False,
-                 gn_eps: float = 1e-5, init_std: float = 0.02):
+                 gn_eps: float = 1e-5, init_std: float = 0.02, n_kv_head: int | None = None):
         super().__init__()
         if variant not in VARIANTS:
             raise ValueError(f"unknown attention variant {variant!r}")
         if d_model % n_head:
             raise ValueError("d_model must be a multiple of n_head")
+        n_kv_head = n_head if n_kv_head is None else n_kv_head
+        if n_kv_head < 1 or n_head % n_kv_head:
+            raise ValueError("n_head must be a multiple of n_kv_head")
         self.d_model, self.n_head, self.d_head = d_model, n_head, d_model // n_head
+        self.n_kv_head = n_kv_head
         if self.d_head not in (64, 128):
             raise ValueError("the CUDA op supports head_dim 64 and 128")
         self.variant, self.group_norm, self.gn_eps = variant, group_norm, gn_eps
-        for name in ("wq", "wk", "wv", "wo"):
-            self.register_parameter(name, nn.Parameter(torch.randn(d_model, d_model) * init_std))
+        d_kv = n_kv_head * self.d_head
+        for name, d_out in (("wq", d_model), ("wk", d_kv), ("wv", d_kv), ("wo", d_model)):
+            self.register_parameter(name, nn.Parameter(torch.randn(d_model, d_out) * init_std))
         if variant == "sb_remainder_bias":
             self.r = nn.Parameter(torch.zeros(n_head, self.d_head))
         if group_norm:
@@ -65,9 +76,11 @@ class StickBreakingAttention(nn.Module):
     def forward(self, x):
         """x (B, L, d_model) -> (B, L, d_model)."""
         B, L, _ = x.shape
-        H, dh = self.n_head, self.d_head
-        split = lambda t: t.view(B, L, H, dh)  # noqa: E731
-        q, k, v = (split(x @ w) for w in (self.wq, self.wk, self.wv))
+        H, dh, Hkv = self.n_head, self.d_head, self.n_kv_head
+        q = (x @ self.wq).view(B, L, H, dh)
+        k, v = ((x @ w).view(B, L, Hkv, dh) for w in (self.wk, self.wv))
+        if Hkv != H:  # grouped-query: query head h reads key/value head h // (H / Hkv)
+            k, v = (t.repeat_interleave(H // Hkv, dim=2) for t in (k, v))
         # (B, H, L, d) views of the (B, L, H, d) projections: the op takes any strides
         # with a contiguous head_dim
         qh, kh, vh = (t.to(torch.bfloat16).transpose(1, 2) for t in (q, k, v))
@@ -88,10 +101,12 @@ class StickBreakingAttention(nn.Module):
 
 
 class SBBlock(nn.Module):
-    def __init__(self, d_model, n_head, d_inter, variant="sb", group_norm=False, init_std=0.02):
+    def __init__(self, d_model, n_head, d_inter, variant="sb", group_norm=False, init_std=0.02,
+                 n_kv_head=None):
         super().__init__()
         self.ln1 = nn.LayerNorm(d_model, eps=1e-5)
-        self.attn = StickBreakingAttention(d_model, n_head, variant, group_norm, init_std=init_std)
+        self.attn = StickBreakingAttention(d_model, n_head, variant, group_norm, init_std=init_std,
+                                           n_kv_head=n_kv_head)
         self.ln2 = nn.LayerNorm(d_model, eps=1e-5)
         self.w1 = nn.Parameter(torch.randn(d_model, d_inter) * init_std)
         self.w2 = nn.Parameter(torch.randn(d_inter, d_model) * init_std)
@@ -105,11 +120,11 @@ class SBTransformer(nn.Module):
     """Decoder-only stack: tokens (B, L) int64 -> logits (B, L, vocab)."""
 
     def __init__(self, vocab_size, n_layer, d_model, n_head, d_inter, variant="sb",
-                 group_norm=False, init_std=0.02):
+                 group_norm=False, init_std=0.02, n_kv_head=None):
         super().__init__()
         self.embed = nn.Parameter(torch.randn(vocab_size, d_model) * init_std)
-        self.layers = nn.ModuleList(SBBlock(d_model, n_head, d_inter, variant, group_norm, init_std)
-                                    for _ in range(n_layer))
+        self.layers = nn.ModuleList(SBBlock(d_model, n_head, d_inter, variant, group_norm, init_std,
+                                            n_kv_head) for _ in range(n_layer))
         self.final_norm = nn.LayerNorm(d_model, eps=1e-5)
         self.head = nn.Parameter(torch.randn(d_model, vocab_size) * init_std)
 

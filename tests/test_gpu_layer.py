@@ -97,3 +97,48 @@ def test_decoder_stack_matches_reference():
     assert errs["logits"] < TOL_OUT
     for k, e in errs.items():
         assert e < TOL_GRAD, (k, e)
+
+
+def test_gqa_shapes_and_validation():
+    """Grouped-query layout (CPU): wk / wv project to n_kv_head heads."""
+    from paper_2410_17980_b200.layer import StickBreakingAttention
+    a = StickBreakingAttention(512, 4, n_kv_head=2)
+    assert tuple(a.wq.shape) == (512, 512) and tuple(a.wk.shape) == (512, 256)
+    assert tuple(a.wv.shape) == (512, 256) and a.n_kv_head == 2
+    with pytest.raises(ValueError):
+        StickBreakingAttention(512, 4, n_kv_head=3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["sb", "sb_remainder"])
+def test_gqa_equals_mha_with_shared_kv(variant):
+    """A grouped-query sublayer (12 query heads over 4 key/value heads, as the
+    paper's 1.2B model) gives bit-identical outputs to the multi-head sublayer whose
+    key/value weights repeat each group's columns, and its wk / wv gradients are the
+    group sums of the multi-head ones."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2410_17980_b200.layer import StickBreakingAttention
+    torch.manual_seed(0)
+    H, Hkv, dh, L = 12, 4, 64, 320
+    d = H * dh
+    gqa = StickBreakingAttention(d, H, variant, n_kv_head=Hkv).cuda()
+    mha = StickBreakingAttention(d, H, variant).cuda()
+    rep = lambda w: w.view(d, Hkv, 1, dh).expand(d, Hkv, H // Hkv, dh).reshape(d, d)  # noqa: E731
+    with torch.no_grad():
+        mha.wq.copy_(gqa.wq)
+        mha.wo.copy_(gqa.wo)
+        mha.wk.copy_(rep(gqa.wk))
+        mha.wv.copy_(rep(gqa.wv))
+    x = torch.randn(2, L, d, device="cuda")
+    dy = torch.randn(2, L, d, device="cuda")
+    yg, ym = gqa(x), mha(x)
+    assert torch.equal(yg, ym)
+    yg.backward(dy)
+    ym.backward(dy)
+    torch.cuda.synchronize()
+    for n in ("wk", "wv"):
+        gm = getattr(mha, n).grad.view(d, Hkv, H // Hkv, dh).sum(2).reshape(d, Hkv * dh)
+        gg = getattr(gqa, n).grad
+        assert rel_to_max(gg.double().cpu().numpy(), gm.double().cpu().numpy()) < 1e-5, n
+    assert torch.allclose(gqa.wq.grad, mha.wq.grad, rtol=1e-5, atol=1e-6)

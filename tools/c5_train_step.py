@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--layers", type=int, default=24)
     ap.add_argument("--d-model", type=int, default=2048)
     ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--kv-heads", type=int, default=0,
+                    help="grouped-query key/value heads (0: = heads; the paper's 1.2B model: "
+                         "--d-model 1536 --heads 12 --kv-heads 4)")
     ap.add_argument("--d-inter", type=int, default=8192)
     ap.add_argument("--vocab", type=int, default=32768)
     ap.add_argument("--seq", type=int, default=4096)
@@ -56,7 +59,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     torch.manual_seed(0)
-    model = SBTransformer(a.vocab, a.layers, a.d_model, a.heads, a.d_inter).to(dev)
+    model = SBTransformer(a.vocab, a.layers, a.d_model, a.heads, a.d_inter,
+                          n_kv_head=a.kv_heads or None).to(dev)
     N = n_params(model)
     flops_tok = train_flops_per_token(model, a.seq)
     net = model
@@ -94,7 +98,8 @@ def main():
     ms = ms.item()
     tok = world * a.batch * a.seq
     res = {"workload": f"C5: SBTransformer {N / 1e9:.2f}B params (d={a.d_model}, {a.heads} heads "
-                       f"x {a.d_model // a.heads}, {a.layers} layers, d_inter={a.d_inter}, "
+                       f"x {a.d_model // a.heads}{f' over {a.kv_heads} kv heads' if a.kv_heads else ''}, "
+                       f"{a.layers} layers, d_inter={a.d_inter}, "
                        f"vocab={a.vocab}), L={a.seq}, {a.batch} seq/GPU, synthetic tokens, "
                        f"bf16 autocast + fp32 AdamW (fused)",
            "n_gpus": world, "parallelism": f"dp{world} (DDP over NCCL)" if world > 1 else "1 GPU",
