@@ -1,0 +1,23 @@
+#!/usr/bin/env python3
+"""Small forward + both backward modes (skip off and on, d = 64 and 128, tails) for
+compute-sanitizer (GPU only):
+
+    for t in memcheck racecheck synccheck; do
+      compute-sanitizer --tool $t python tools/sanitize_case.py; done
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2410_17980_b200 as sb  # noqa: E402
+from tests.gpu_util import make_qkv  # noqa: E402
+
+for (B, H, L, d, skip) in [(1, 2, 320, 128, False), (1, 2, 256, 64, True)]:
+    q, k, v, do = make_qkv(B, H, L, d, seed=1)
+    o, lr, st, cache = sb.blocked_forward(q, k, v, skip=skip)
+    for store in (False, True):
+        dq, dk, dv, _ = sb.blocked_backward_twophase(cache, do, store_tiles=store)
+    torch.cuda.synchronize()
+print("sanitizer case ok")
