@@ -31,8 +31,8 @@
 
 namespace sb {
 
-constexpr int kBwdThreads = 12 * 32;
-constexpr bool kPingPongQ = true;  // phase 1: the warpgroups take turns at the recompute  // WG0, WG1 stick; WG2 = producer, MMA0, MMA1, idle
+constexpr int kBwdThreads = 12 * 32;  // WG0, WG1 stick; WG2 = producer, MMA0, MMA1, idle
+constexpr bool kPingPongQ = true;  // phase 1: the warpgroups take turns at the recompute
 // setmaxnreg only redistributes the CTA's launch allocation (384 threads x 168
 // registers): 128 x low + 256 x high <= 384 x 168, otherwise .inc blocks forever.
 constexpr int kRegsLaunch = 168;
@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // bar 2, recomputes, arrives on bar 1; then WG0 waits bar 1, recomputes,
     // arrives on bar 2.  Both run max(n0, n1) rounds per item (a warpgroup without
     // a tile in a round passes straight through).  (WG1 first: 0.94-0.95 ms vs
-    // 0.96-0.97 with WG0 first.)
+    // 0.96-0.97 with WG0 first; letting WG0 skip its trailing rounds and go on to
+    // its epilogue: 1.14 ms, the turn order then drifts.)
     const uint32_t bar_mine = 1 + w, bar_other = 2 - w;
     auto pp_round_pass = [&]() {
       named_bar_sync(bar_mine, 256);
