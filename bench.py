@@ -12,10 +12,11 @@ max-over-ranks of the timings.  One step = sb_fwd + sb_bwd (phase 1 + phase 2).
 value   = whole-job tokens/s with inputs resident in HBM (CUDA events, max over ranks).
 e2e     = the same metric through the public autograd op stickbreaking_attention()
           with q, k, v, dO copied host->device from pinned memory every step and the
-          step's result (a fp32 checksum of o, dq, dk, dv) read back device->host.
+          step's results (o, dq, dk, dv) read back device->host every step.
 roofline = the dominant kernel's algorithmic tensor FLOPs per launch / its CUDA-event
-          duration, against MEASURED_PEAKS.json bf16 (sustained: kernels timed inside
-          a long step).
+          duration, against MEASURED_PEAKS.json bf16: the burst peak when the run held
+          its SM clock at max without a power cap, else the sustained one (both
+          fractions are reported).
 cpu_baseline = the CPU oracle port (oracle/, C, float32, all host threads) on a bounded
           sample of the same workload (rank 0, N=1 only).
 --impl reference times that CPU port as the reference arm (no GPU work).
@@ -132,28 +133,40 @@ def cpu_sample(n_units=None, threads=None):
 
 
 def run_reference(args, rank, world):
-    """Reference arm: the reference's CPU algorithm (oracle C port) on the host cores."""
+    """Reference arm: the reference's CPU algorithm (oracle C port) on the host cores.
+
+    One step = one bounded sample of C2: as many (b, h) units as host threads, each
+    unit a full L=4096 d=128 fwd + two-phase bwd in f32.  value = tokens/s of that
+    sample (units are independent and equal-cost, so it is the whole-batch rate);
+    ms_per_step is the sample's measured wall time (not extrapolated)."""
     if rank != 0:
         return
     import oracle
     oracle.build()
     threads = oracle.n_threads_default()
-    units = max(1, min(threads, B * H))
-    for _ in range(args.warmup):
-        pass  # the CPU port has no warm-up state worth paying for; keep the run short
-    vals = []
+    units = max(1, min(args.cpu_units or threads, B * H))
+    t_all = time.perf_counter()
+    for _ in range(max(1, args.warmup)):  # same-size samples, untimed
+        cpu_sample(units, threads)
+        if time.perf_counter() - t_all > 60:
+            break
+    n_warm = _ + 1
+    vals, secs = [], []
     t_all = time.perf_counter()
     for _ in range(max(1, args.steps)):
         s = cpu_sample(units, threads)
         vals.append(s["value"])
+        secs.append(s["seconds_per_unit"] * units)
         if time.perf_counter() - t_all > 150:
             break
     value = statistics.median(vals)
-    ms = B * L / value * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": len(vals), "warmup": args.warmup, "ms_per_step": ms,
+            "steps": len(vals), "warmup": n_warm, "ms_per_step": statistics.median(secs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD + " (CPU, bounded sample)"},
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD + " (CPU)",
+                       "step": f"one sample of {units} of the {B * H} (b,h) units, one per host "
+                               f"thread; tokens/s = units/{B * H} x {B * L} tokens / sample time"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": s["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -226,14 +239,23 @@ def main():
 
     M_elems = sb.ops._lib.load().sb_snapshot_elems(
         __import__("ctypes").byref(sb.ops._params(q, 1.0 / math.sqrt(D), False, 1e-6)))
-    step.out = (torch.empty(M_elems, device=dev, dtype=torch.float32), torch.empty_like(q),
-                torch.empty_like(q), torch.empty_like(q))
     # dZ tile workspace of the store-mode backward (shared by the two phase launches)
     _, _, _, cache0 = sb.blocked_forward(q, k, v, counters=False)
     n_tiles_bytes = sb.ops.tile_workspace_bytes(cache0)
     step.tiles = (torch.empty(n_tiles_bytes, device=dev, dtype=torch.uint8)
-                  if n_tiles_bytes <= sb.ops.TILE_WORKSPACE_MAX_BYTES else None)
+                  if n_tiles_bytes <= sb.ops.workspace_cap_bytes(dev) else None)
     del cache0
+    # store mode needs no N snapshots (phase 2 reads dZ); recompute mode does
+    step.out = (None if step.tiles is not None else
+                torch.empty(M_elems, device=dev, dtype=torch.float32),
+                torch.empty_like(q), torch.empty_like(q), torch.empty_like(q))
+    snap_bytes = M_elems * 4
+    intermediates = {
+        "M_bytes": snap_bytes, "N_bytes": 0 if step.tiles is not None else snap_bytes,
+        "dZ_workspace_bytes": n_tiles_bytes if step.tiles is not None else 0,
+        "note": "per step: M written by the forward and read by both backward phases; N only "
+                "in recompute mode; the store-mode dZ workspace is written by phase 1 and read "
+                "by phase 2 (bf16, O(L^2)); an inference forward (no autograd) writes no M"}
 
     for _ in range(W):
         step()
@@ -279,17 +301,29 @@ def main():
     exec_flops = 5 * G + p2_exec
     tflops = world * alg_flops * K / (total_ms / 1e3) / 1e12
     burst, sustained, peak_kind = load_peaks()
+    # Denominator: the burst peak applies when this run held its clock (median SM clock
+    # within 5% of max and no power cap), the sustained one (measured at a power-capped
+    # 1327 MHz median) otherwise.  Both fractions are reported.
+    held = (clk.get("sm_mhz") and clk.get("sm_max_mhz")
+            and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"] and "sw_power_cap" not in clk["reasons"])
+    peak = burst if held else sustained
     kernels = {"sb_fwd_pp_kernel": (fwd_ms, 2 * G, 2 * G), "sb_bwd_q_kernel": (p1_ms, 3 * G, 3 * G),
                ("sb_bwd_kvs_kernel" if store else "sb_bwd_kv_kernel"): (p2_ms, 2 * G, p2_exec)}
     dom = max(kernels, key=lambda n: kernels[n][0])
     d_ms, d_alg, d_exec = kernels[dom]
     achieved = d_alg / (d_ms / 1e3) / 1e12
-    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": sustained,
-                "unit": "TFLOP/s", "frac": achieved / sustained,
-                "peak_kind": f"{peak_kind} bf16 sustained (burst {burst})",
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_kind": (f"{peak_kind} bf16 dense {'burst' if held else 'sustained'} "
+                              f"(clock {'held at max, no power cap' if held else 'below max or power-capped'})"),
+                "frac_burst": achieved / burst, "frac_sustained": achieved / sustained,
                 "executed_tflops": d_exec / (d_ms / 1e3) / 1e12, "traffic": None,
                 "per_kernel_ms": {n: round(v[0], 4) for n, v in kernels.items()},
-                "step_frac_of_peak": tflops / world / sustained}
+                "per_kernel_frac_burst": {n: round(v[1] / (v[0] / 1e3) / 1e12 / burst, 4)
+                                          for n, v in kernels.items()},
+                "step_frac_of_peak": tflops / world / peak,
+                "step_frac_burst": tflops / world / burst,
+                "step_frac_sustained": tflops / world / sustained}
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             roofline["traffic"] = json.load(f).get(dom)
@@ -301,15 +335,21 @@ def main():
     if not args.no_e2e:
         # Inputs of every step come from pinned host memory; step i+1's H2D copy runs
         # on a copy stream while step i computes (double-buffered prefetch, as a data
-        # loader would).  Each step ends with a 16-byte D2H read of its checksums.
+        # loader would).  Each step's results (o, dq, dk, dv: 512 MiB) go back to
+        # pinned host memory on a third stream, overlapped with the next step; the
+        # timed region ends when the last step's results are on the host.
         hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, d_o))
-        hres = torch.empty(2, 4, dtype=torch.float32).pin_memory()
+        hout = [[torch.empty(q.shape, dtype=q.dtype).pin_memory() for _ in range(4)]
+                for _ in range(2)]
         h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
-        d2h = hres[0].numel() * hres.element_size()
+        d2h = sum(x.numel() * x.element_size() for x in hout[0])
         sets = [[torch.empty_like(q) for _ in range(4)] for _ in range(2)]
         copy_stream = torch.cuda.Stream(device=dev)
+        back_stream = torch.cuda.Stream(device=dev)
         landed = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
+        computed = [torch.cuda.Event() for _ in range(2)]
+        read_back = [torch.cuda.Event() for _ in range(2)]
 
         def prefetch(i):
             with torch.cuda.stream(copy_stream):
@@ -319,7 +359,7 @@ def main():
                 landed[i % 2].record(copy_stream)
 
         def e2e_run(n):
-            for c in consumed:
+            for c in consumed + read_back:
                 c.record(stream)
             prefetch(0)
             for i in range(n):
@@ -330,14 +370,20 @@ def main():
                 qq, kk, vv = (x.requires_grad_(True) for x in (bq, bk, bv))
                 o = sb.stickbreaking_attention(qq, kk, vv)
                 o.backward(bdo)
-                res = torch.stack([o.sum(dtype=torch.float32), qq.grad.sum(dtype=torch.float32),
-                                   kk.grad.sum(dtype=torch.float32),
-                                   vv.grad.sum(dtype=torch.float32)])
-                hres[i % 2].copy_(res, non_blocking=True)
+                res = (o.detach(), qq.grad, kk.grad, vv.grad)
                 consumed[i % 2].record(stream)
+                computed[i % 2].record(stream)
+                with torch.cuda.stream(back_stream):
+                    back_stream.wait_event(computed[i % 2])
+                    back_stream.wait_event(read_back[i % 2])  # host buffers of step i-2 free
+                    for hx, x in zip(hout[i % 2], res):
+                        hx.copy_(x, non_blocking=True)
+                        x.record_stream(back_stream)
+                    read_back[i % 2].record(back_stream)
                 for x in (qq, kk, vv):
                     x.grad = None
                     x.requires_grad_(False)
+            stream.wait_stream(back_stream)
 
         e2e_run(2)
         torch.cuda.synchronize()
@@ -357,8 +403,10 @@ def main():
                "ms_per_step": te.item() / Ke,
                "api": "stickbreaking_attention(q,k,v) + o.backward(dO); q,k,v,dO copied from "
                       "pinned host memory every step (next step's copy overlapped with this "
-                      "step's compute on a copy stream), checksums read back every step",
-               "h2d_gbps": h2d * Ke / (te.item() / 1e3) / 1e9}
+                      "step's compute on a copy stream); o,dq,dk,dv copied back to pinned host "
+                      "memory every step on a third stream",
+               "h2d_gbps": h2d * Ke / (te.item() / 1e3) / 1e9,
+               "d2h_gbps": d2h * Ke / (te.item() / 1e3) / 1e9}
 
     # ---------------------------------------------------------------- comparators
     comparator = None
@@ -413,7 +461,8 @@ def main():
         "tflops": tflops, "tflops_note": "algorithmic 7*B*H*L^2*d per step (FA causal convention)",
         "executed_tflops": world * exec_flops * K / (total_ms / 1e3) / 1e12,
         "ms": {"fwd": fwd_ms, "bwd_phase1": p1_ms, "bwd_phase2": p2_ms},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 3 * K,
+        "roofline": roofline, "intermediates": intermediates, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": 3 * K,
         "clocks": clk, "comparator": comparator,
     }
     if rank == 0:

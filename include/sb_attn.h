@@ -84,7 +84,10 @@ int sb_varlen_elems(const sb_params_t* p, const int32_t* cu_seqlens_host, size_t
  * the remaining stick mass, RowLogAccumulator.a), first_kb [B,H,nb] int32
  * (TileStats.first_kb), M (snapshot array, opaque; required by sb_bwd),
  * tile_counters (nullable) += {visited} (TileStats.visited).  stream is a
- * cudaStream_t (NULL = legacy default stream). */
+ * cudaStream_t (NULL = legacy default stream).
+ * M may be NULL: a forward for inference that writes no snapshots, the
+ * reference's blocked_forward(two_phase=False) (blocked.py:136, :163, :188);
+ * results are identical, only sb_bwd cannot follow it. */
 int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, void* o,
            float* log_rem, int32_t* first_kb, float* M, unsigned long long* tile_counters,
            void* stream);
@@ -92,7 +95,8 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
 /* Two-phase backward.  row_offset (nullable) [B,H,L] float is the per-row
  * offset subtracted from dO.V^T (blocked.py:241-242, :274-276); N is a
  * caller-provided snapshot workspace (sb_snapshot_elems floats).  Writes dq,
- * dk, dv (bf16, q's layout). */
+ * dk, dv (bf16, q's layout).  log_rem is unused (the backward reads the per-tile
+ * M snapshots) and may be NULL. */
 int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
            const float* row_offset, const float* log_rem, const int32_t* first_kb,
            const float* M, float* N, void* dq, void* dk, void* dv, void* stream);
@@ -108,12 +112,16 @@ int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void*
 /* Store mode of the backward.  Bytes of the dZ tile workspace: phase 1 writes
  * every 128-row x 64-key dZ tile it computes (bf16, 16 KB each; per (b,h) unit
  * n_qt*(n_qt+1) tiles, n_qt = ceil(L/128)) and phase 2 reads them back instead of
- * recomputing dO.V^T and dZ (same results, bit for bit).  cu_seqlens_host: host
- * copy of the offsets for packed varlen batches, else NULL. */
+ * recomputing dO.V^T and dZ (same results, bit for bit), plus 256 bytes of
+ * work-queue counters.  cu_seqlens_host: host copy of the offsets for packed
+ * varlen batches, else NULL. */
 size_t sb_bwd_tile_bytes(const sb_params_t* p, const int32_t* cu_seqlens_host);
 
 /* sb_bwd_phase with an optional dZ tile workspace (ztiles: device, 128-byte
- * aligned, ztiles_bytes >= sb_bwd_tile_bytes; NULL = recompute mode). */
+ * aligned, ztiles_bytes >= sb_bwd_tile_bytes; NULL = recompute mode).  In store
+ * mode N may be NULL (phase 2 reads dZ, not the b snapshots) and is not written.
+ * Uniform batches get SB_ERR_SHAPE for a short workspace; for varlen batches
+ * the caller must size it with sb_bwd_tile_bytes(p, cu_seqlens_host). */
 int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
               const float* row_offset, const float* log_rem, const int32_t* first_kb,
               const float* M, float* N, void* dq, void* dk, void* dv, void* ztiles,

@@ -13,17 +13,16 @@
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // function-local static: initialised once, thread-safe (C++11)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
   return fn;
 }
 
@@ -77,6 +76,8 @@ int validate(const sb_params_t* p) {
   if (p->head_dim != 64 && p->head_dim != 128) return SB_ERR_UNSUPPORTED;
   if (p->skip && !(p->skip_eps == 0.0f || (p->skip_eps > 0.0f && p->skip_eps < 1.0f)))
     return SB_ERR_SKIP_EPS;
+  // the skip-on forward packs a warpgroup's stop tile into 13 bits (sb_fwd_pp.cu)
+  if (p->skip && (p->seqlen + 63) / 64 >= 8192) return SB_ERR_UNSUPPORTED;
   for (int64_t s : {p->stride_l, p->stride_h, p->stride_b})
     if (s < 0) return SB_ERR_SHAPE;
   if ((p->stride_l * 2) % 16 || (p->heads > 1 && (p->stride_h * 2) % 16) ||
@@ -150,7 +151,9 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
            void* stream) {
   int st = validate(p);
   if (st) return st;
-  if (!q || !k || !v || !o || !log_rem || !first_kb || !M) return SB_ERR_NULL;
+  // M == NULL: forward for inference, no snapshots (blocked_forward(two_phase=False),
+  // blocked.py:136, :163, :188); the backward then cannot run on this forward
+  if (!q || !k || !v || !o || !log_rem || !first_kb) return SB_ERR_NULL;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return SB_ERR_UNSUPPORTED;
   CUtensorMap tq, tk, tv;
   if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tk, k, p, 64)) ||
@@ -166,7 +169,7 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
   a.log_eps = std::log(eps);
   a.trace = g_trace;
-  a.sched = reinterpret_cast<unsigned*>(M);
+  a.sched = reinterpret_cast<unsigned*>(M);  // NULL: items dealt statically
   // the persistent ping-pong product-form kernel, with the exact skip decisions
   // when skip is on; SB_FWD_SKIP_V1=1 selects the older all-log-space skip kernel
   // (sb_fwd.cu, kept as a cross-check)
@@ -175,7 +178,7 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
     const char* e = std::getenv("SB_FWD_SKIP_V1");
     return e && e[0] == '1';
   }();
-  int rc = (p->skip && v1) ? sb::fwd_dispatch(p->head_dim, true, tq, tk, tv, a, st_)
+  int rc = (p->skip && v1 && M) ? sb::fwd_dispatch(p->head_dim, true, tq, tk, tv, a, st_)
                            : sb::fwd_pp_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a, st_);
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
@@ -199,7 +202,8 @@ size_t sb_bwd_tile_bytes(const sb_params_t* p, const int32_t* cu) {
       tiles += (size_t)p->heads * nq * (nq + 1);
     }
   }
-  return tiles * sb::kZTileBytes;
+  // + the backward's work-queue counters after the last tile (store mode needs no N)
+  return tiles * sb::kZTileBytes + sb::kZTailBytes;
 }
 
 int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void* v,
@@ -217,23 +221,29 @@ int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v,
   if (phases < 1 || phases > 3) return SB_ERR_SHAPE;
   int st = validate(p);
   if (st) return st;
-  (void)log_rem;  // the backward reads the per-tile M snapshots, not the final a
-  if (!q || !k || !v || !d_o || !first_kb || !N || !dq || !dk || !dv) return SB_ERR_NULL;
+  (void)log_rem;  // unused (may be NULL): the backward reads the per-tile M snapshots
+  const bool store = ztiles != nullptr;
+  // N (the b snapshots) is read only by the recompute-mode phase 2: store mode takes
+  // dZ from the tile workspace instead and needs no N
+  if (!q || !k || !v || !d_o || !first_kb || !dq || !dk || !dv || (!N && !store))
+    return SB_ERR_NULL;
   if (!M) return SB_ERR_NULL;  // blocked.py:315-316: M snapshots missing
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(d_o) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return SB_ERR_UNSUPPORTED;
+  if (store) {
+    // uniform batches are checked here; a varlen caller sizes the workspace with
+    // sb_bwd_tile_bytes(p, host cu_seqlens) (the device offsets are not read here)
+    if (ztiles_bytes < sb::kZTailBytes + sb::kZTileBytes) return SB_ERR_SHAPE;
+    if (!p->cu_seqlens && ztiles_bytes < sb_bwd_tile_bytes(p, nullptr)) return SB_ERR_SHAPE;
+    if (reinterpret_cast<uintptr_t>(ztiles) & 127) return SB_ERR_UNSUPPORTED;
+  }
   CUtensorMap tq, tdo, tk, tv, tz;
   if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
       (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)))
     return st;
-  const bool store = ztiles != nullptr;
   std::memset(&tz, 0, sizeof(tz));
-  if (store) {
-    if (ztiles_bytes < sb_bwd_tile_bytes(p, nullptr) && !p->cu_seqlens) return SB_ERR_SHAPE;
-    if (reinterpret_cast<uintptr_t>(ztiles) & 127) return SB_ERR_UNSUPPORTED;
-    if ((st = make_tile_map(&tz, ztiles, ztiles_bytes))) return st;
-  }
+  if (store && (st = make_tile_map(&tz, ztiles, ztiles_bytes - sb::kZTailBytes))) return st;
   sb::BwdArgs a;
   a.g = geom(p);
   a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
@@ -244,7 +254,11 @@ int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v,
   a.M = M;
   a.N = N;
   a.trace = g_trace;
-  a.sched = reinterpret_cast<unsigned*>(N);
+  // work-queue counters: the N header, or (store mode) the workspace's tail
+  a.sched = store ? reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(ztiles) + ztiles_bytes -
+                                                sb::kZTailBytes)
+                  : reinterpret_cast<unsigned*>(N);
+  if (store) a.N = nullptr;
   int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, a, phases, store,
                             reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
@@ -265,7 +279,8 @@ const char* sb_status_string(int s) {
   }
 }
 
-int sb_version(void) { return 3; }  // 2: packed varlen; 3: dZ tile workspace (sb_bwd_ws)
+int sb_version(void) { return 4; }  // 2: packed varlen; 3: dZ tile workspace (sb_bwd_ws);
+                                    // 4: M-free forward, N-free store mode
 
 #ifdef SB_TRACE
 // debug builds only: device buffer of kTraceCtas*4*64*16 uint32 clock stamps

@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float off =
           (args.row_offset && row_valid) ? args.row_offset[u.rem_off + row * u.rem_stride] : 0.0f;
       const float* Mrow = args.M + u.m_off + (r & 63);
-      float* Nrow = args.N + u.m_off + (r & 63);
+      float* Nrow = kStoreZ ? nullptr : args.N + u.m_off + (r & 63);  // store mode: no N
       const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
       auto tile_of = [&](int kb) -> int64_t {  // snapshot slot (row 0 of the unit if not live)
         const bool lv = row_valid && kb >= my_first && kb <= my_qb;
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_arrive(wempty);
         if (tr) SB_TR(args, w, gi, 3);
         uint32_t pk[32];
-        if (live) Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
+        if (!kStoreZ && live) Nrow[t] = bsum;  // b in effect for this tile (blocked.py:353)
         const float bnext = dz_row(s, sg, live ? bsum : 0.0f, pk);
         bsum = live ? bnext : bsum;
         if (tr) SB_TR(args, w, gi, 4);

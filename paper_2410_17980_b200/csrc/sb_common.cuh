@@ -54,6 +54,8 @@ struct Unit {
 // (the 128B-swizzled smem image, as the MMA reads it).
 __device__ __forceinline__ int64_t ztile(int qt, int kb) { return (int64_t)qt * (qt + 1) + kb; }
 constexpr int kZTileBytes = kTileM * kBlock * 2;
+// the workspace ends with the backward's work-queue counters (store mode has no N)
+constexpr int kZTailBytes = 256;
 
 __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
   Unit u;
@@ -127,11 +129,13 @@ __device__ __forceinline__ void sched_init(const SchedRing& q, int consumers) {
     mbar_init(q.empty + i, consumers);
   }
 }
-// producer warp, k-th item (whole warp; returns the index to every lane)
+// producer warp, k-th item (whole warp; returns the index to every lane).  With
+// ctr == nullptr (a forward without the M array, whose header holds the counter)
+// the items are dealt statically: CTA c takes c, c + grid, c + 2 grid, ...
 __device__ __forceinline__ int sched_produce(const SchedRing& q, int k, unsigned* ctr, int n_items) {
   int idx = 0;
   if ((threadIdx.x & 31) == 0) {
-    idx = (int)atomicAdd(ctr, 1u);
+    idx = ctr ? (int)atomicAdd(ctr, 1u) : (int)(blockIdx.x + (unsigned)k * gridDim.x);
     if (idx >= n_items) idx = -1;
     if (k >= 4) mbar_wait(q.empty + (k & 3), ((k >> 2) - 1) & 1);
     q.slot[k & 3] = idx;

@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           bool stop = false;
           const long long t0 = clock64();
           for (;;) {
-            if (clock64() - t0 > (1ll << 33)) __trap();  // deadlock: fail loudly
+            if (watchdog_expired(t0)) __trap();  // deadlock: fail loudly (sm100.cuh)
             if (j > 0 && stop_of(0, ni) <= j && (!it.has1 || stop_of(1, ni) <= j)) {
               stop = true;
               break;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             if (j >= n) return n;
           }
           if (kv) break;
-          if (clock64() - t0 > (1ll << 33)) __trap();  // deadlock: fail loudly
+          if (watchdog_expired(t0)) __trap();  // deadlock: fail loudly (sm100.cuh)
         }
         if (leader) mbar_arrive(bar_kvempty + s);
         __syncwarp();
@@ -405,7 +405,8 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
       const bool row_valid = row < u.L;
-      float* Mrow = args.M + u.m_off + (r & 63);
+      // M == nullptr: a forward for inference (no backward), no snapshots written
+      float* Mrow = args.M ? args.M + u.m_off + (r & 63) : nullptr;
       const int kbhi = w ? it.kbhi1 : it.kbhi0;
       const int n_w = kbhi + 1;
       float a2 = 0.0f;  // running log2 remaining mass
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             // exact lt sum first (t left in s[]), then the product form from t
             const float tot = diag ? exact_lt_row<true>(s, sl2, lim) : exact_lt_row<false>(s, sl2, lim);
             slow = !batched_from_t(s, pk, ex2(a2));
-            if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
+            if (row_valid && Mrow) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
             a_d += (double)tot * (double)kLn2;
             a2 = (float)(a_d * 1.4426950408889634);
             lowest = kb;
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
             slow = diag ? !batched_row<true>(s, pk, sl2, lim, Q, Dhi, Dlo)
                         : !batched_row<false>(s, pk, sl2, kBlock, Q, Dhi, Dlo);
-            if (row_valid) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
+            if (row_valid && Mrow) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
             if (!slow) a2 -= lg2(Dhi) + lg2(Dlo);
           }
         } else {
@@ -610,7 +611,8 @@ static int launch_fwd_pp(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   auto kern = sb_fwd_pp_kernel<D, kSkip>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return (int)e;
-  if ((e = cudaMemsetAsync(a.sched, 0, sizeof(unsigned), stream)) != cudaSuccess) return (int)e;
+  if (a.sched && (e = cudaMemsetAsync(a.sched, 0, sizeof(unsigned), stream)) != cudaSuccess)
+    return (int)e;
   // persistent: one CTA per SM (fewer if there are fewer work items)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

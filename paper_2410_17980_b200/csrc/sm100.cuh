@@ -50,15 +50,23 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Blocking wait.  A wait still pending after 2^33 SM clocks (~4 s; a whole
-// kernel takes milliseconds) is a deadlock: trap so the launch fails loudly
-// instead of hanging the GPU.
+// Deadlock watchdog of the pipeline waits: a wait still pending after
+// 2^SB_WATCHDOG_LOG2 SM clocks (default 2^36, ~35 s at 1.965 GHz; a whole kernel
+// takes milliseconds) traps so the launch fails loudly instead of hanging the
+// GPU.  The bound is far above any stall from outside the kernel (time-slicing
+// between processes, a profiler's replay); -DSB_WATCHDOG_LOG2=0 compiles it out.
+#ifndef SB_WATCHDOG_LOG2
+#define SB_WATCHDOG_LOG2 36
+#endif
+__device__ __forceinline__ bool watchdog_expired(long long t0) {
+  return SB_WATCHDOG_LOG2 > 0 && clock64() - t0 > (1ll << (SB_WATCHDOG_LOG2 & 63));
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && clock64() - t0 > (1ll << 33)) __trap();
+    if ((++n & 1023u) == 0 && watchdog_expired(t0)) __trap();
   }
 }
 

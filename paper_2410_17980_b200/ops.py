@@ -134,9 +134,28 @@ def _check_qkv(q, k, v, varlen=False):
         raise ValueError(f"head_dim {q.shape[-1]} unsupported (64 or 128)")
 
 
+def _dense(t) -> bool:
+    """Non-overlapping and dense: some order of the dims has contiguous strides
+    (a BLHD view of BHLD storage, or the reverse), so empty_like(t) keeps t's
+    strides and outputs allocated that way are addressed exactly like t."""
+    expected = 1
+    for i in sorted(range(t.dim()), key=lambda i: (t.stride(i), t.size(i))):
+        if t.size(i) == 1:
+            continue
+        if t.stride(i) != expected:
+            return False
+        expected *= t.size(i)
+    return True
+
+
 def _same_layout(*ts):
+    """q, k, v (and the outputs, allocated like q) must share one strided layout.
+    q is made contiguous unless it is dense with a contiguous last dim and 16-byte
+    aligned: a fused-QKV slice (qkv[:, :, 0] of a (B, L, 3, H, d) tensor) is
+    strided but not dense, and outputs allocated like it would be addressed past
+    their storage."""
     base = ts[0]
-    if base.stride(-1) != 1 or base.data_ptr() % 16:
+    if base.stride(-1) != 1 or base.data_ptr() % 16 or not _dense(base):
         base = base.contiguous()
     out = [base]
     for t in ts[1:]:
@@ -191,7 +210,8 @@ def _varlen_plan(cu_seqlens, q):
     return host, dev, lens, max(lens)
 
 
-def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters):
+def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters,
+                            two_phase=True):
     _check_qkv(q, k, v, varlen=True)
     T, H, d = q.shape
     host, cu, lens, max_L = _varlen_plan(cu_seqlens, q)
@@ -211,7 +231,7 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
     o = torch.empty_like(q)
     log_rem = torch.empty((T, H), device=q.device, dtype=torch.float32)
     first_kb = torch.empty(max(1, n_fkb.value), device=q.device, dtype=torch.int32)
-    M = torch.empty(max(1, n_snap.value), device=q.device, dtype=torch.float32)
+    M = torch.empty(max(1, n_snap.value), device=q.device, dtype=torch.float32) if two_phase else None
     cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
     if max_L > 0:
         _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
@@ -229,11 +249,17 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
 
 def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = False,
                     skip_eps: float | None = None, scale: float | None = None,
-                    counters: bool = True, cu_seqlens: torch.Tensor | None = None):
-    """blocked_forward(two_phase=True) over every (b, h) unit (blocked.py:129-206).
+                    counters: bool = True, cu_seqlens: torch.Tensor | None = None,
+                    two_phase: bool = True):
+    """blocked_forward over every (b, h) unit (blocked.py:129-206).
 
     Returns (o, log_rem, TileStats, BlockedCache).  log_rem is the reference's
     RowLogAccumulator.a (natural log of the remaining stick mass).
+
+    two_phase=False (blocked.py:136, :163, :188) writes no M snapshots (o, log_rem
+    and first_kb are the same bit for bit): a forward for inference, after which
+    the two-phase backward raises ValueError.  (The reference's fused backward
+    does not exist here: SURVEY.md §8(a).)
 
     Varlen: q, k, v (total_tokens, H, d) with cu_seqlens (int32 [n_seq+1]);
     log_rem is then (total_tokens, H), first_kb a flat array packed sequence by
@@ -242,7 +268,8 @@ def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = Fal
     if cu_seqlens is not None:
         if layout is not None:
             raise ValueError("varlen batches are planned per sequence; pass layout=None")
-        return _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters)
+        return _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters,
+                                       two_phase)
     _check_qkv(q, k, v)
     B, H, L, d = q.shape
     if layout is None:
@@ -263,7 +290,8 @@ def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = Fal
     o = torch.empty_like(q)
     log_rem = torch.empty((B, H, L), device=q.device, dtype=torch.float32)
     first_kb = torch.empty((B, H, layout.n_blocks), device=q.device, dtype=torch.int32)
-    M = torch.empty(lib.sb_snapshot_elems(ctypes.byref(p)), device=q.device, dtype=torch.float32)
+    M = (torch.empty(lib.sb_snapshot_elems(ctypes.byref(p)), device=q.device, dtype=torch.float32)
+         if two_phase else None)
     cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
     _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
                           _ptr(first_kb), _ptr(M), _ptr(cnt), _stream()))
@@ -289,6 +317,19 @@ def tile_workspace_bytes(cache: BlockedCache) -> int:
     return int(lib.sb_bwd_tile_bytes(ctypes.byref(p), host))
 
 
+def workspace_cap_bytes(device=None) -> int:
+    """Largest dZ tile workspace the backward allocates on its own: the
+    SB_TILE_WORKSPACE_MAX_GB cap (default 8 GiB), and at most a quarter of the
+    device memory free right now.  Above it the backward runs in recompute mode."""
+    cap = TILE_WORKSPACE_MAX_BYTES
+    try:
+        free, _ = torch.cuda.mem_get_info(device)
+        cap = min(cap, free // 4)
+    except Exception:  # pragma: no cover - no device query possible
+        pass
+    return cap
+
+
 def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | None = None,
                               row_offset=None, *, out=None, phases: int = 3,
                               store_tiles: bool | None = None, tiles=None):
@@ -297,16 +338,17 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     Returns (d_q, d_k, d_v, n_stored_tiles).  row_offset (B, H, L) float32 is
     subtracted from dO.V^T per query row (blocked.py:241-242).
 
-    store_tiles: None = store mode when its workspace fits TILE_WORKSPACE_MAX_BYTES,
+    store_tiles: None = store mode when its workspace fits workspace_cap_bytes(),
     True/False to force.  `tiles` passes a preallocated workspace (uint8 CUDA tensor of
-    tile_workspace_bytes(cache)); callers running the phases one by one must pass the
-    same one to both.
+    at least tile_workspace_bytes(cache) bytes); callers running the phases one by one
+    must pass the same one to both.  Store mode needs no N snapshots (phase 2 reads
+    dZ); recompute mode allocates N (one float per row per tile, like M).
     """
     if layout is not None and layout != cache.layout:
         raise ValueError("layout does not match the one the cache was built with")  # :398-399
     if cache.M is None:
         raise ValueError("two-phase backward needs a forward run with two_phase=True "
-                         "(M snapshots missing)")
+                         "(M snapshots missing)")  # blocked.py:315-316
     q, k, v = cache.q, cache.k, cache.v
     if d_o.shape != v.shape:
         raise ValueError("d_o shape mismatch")
@@ -317,10 +359,6 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     lib = _lib.load()
     p = _params(q, cache.scale, cache.skip, cache.skip_eps, cu_seqlens=cache.cu_seqlens,
                 max_seqlen=cache.max_seqlen)
-    if out is None:  # (N, dq, dk, dv); callers running the phases one by one pass it
-        out = (torch.empty_like(cache.M), torch.empty_like(q), torch.empty_like(q),
-               torch.empty_like(q))
-    N, dq, dk, dv = out
     ro = None
     if row_offset is not None:
         ro = row_offset.to(device=q.device, dtype=torch.float32).contiguous()
@@ -328,15 +366,25 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
             raise ValueError("row_offset must match log_rem: (batch, heads, seq_len), or "
                              "(total_tokens, heads) for varlen")
     if cache.cu_seqlens is not None and cache.max_seqlen == 0:
-        return dq.zero_(), dk.zero_(), dv.zero_(), 0
+        dq, dk, dv = (torch.zeros_like(q) for _ in range(3))
+        return dq, dk, dv, 0
+    need = tile_workspace_bytes(cache)
     if tiles is None:
-        nbytes = tile_workspace_bytes(cache)
-        use = (nbytes <= TILE_WORKSPACE_MAX_BYTES) if store_tiles is None else bool(store_tiles)
-        if use and nbytes > 0:
-            tiles = torch.empty(nbytes, device=q.device, dtype=torch.uint8)
+        use = (need <= workspace_cap_bytes(q.device)) if store_tiles is None else bool(store_tiles)
+        if use and need > 0:
+            tiles = torch.empty(need, device=q.device, dtype=torch.uint8)
+    elif tiles.numel() < need:
+        raise ValueError(f"tile workspace has {tiles.numel()} bytes, the backward needs {need}")
+    store = tiles is not None
+    if out is None:  # (N, dq, dk, dv); callers running the phases one by one pass it
+        out = (None if store else torch.empty_like(cache.M), torch.empty_like(q),
+               torch.empty_like(q), torch.empty_like(q))
+    N, dq, dk, dv = out
+    if N is None and not store:
+        raise ValueError("recompute mode needs an N snapshot buffer")
     nbytes = 0 if tiles is None else tiles.numel()
     _lib.check(lib.sb_bwd_ws(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
-                             _ptr(cache.log_rem), _ptr(cache.first_kb), _ptr(cache.M), _ptr(N),
+                             None, _ptr(cache.first_kb), _ptr(cache.M), _ptr(N),
                              _ptr(dq), _ptr(dk), _ptr(dv), _ptr(tiles), nbytes, int(phases),
                              _stream()))
     n_stored = ((cache.M.numel() - SCHED_HEADER) // DEFAULT_BLOCK if cache.cu_seqlens is not None
@@ -345,28 +393,39 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
 
 
 class _StickBreakingFn(torch.autograd.Function):
-    @staticmethod
-    def forward(ctx, q, k, v, scale, skip, skip_eps, cu_seqlens):
-        o, log_rem, _, cache = blocked_forward(q, k, v, skip=skip, skip_eps=skip_eps,
-                                               scale=scale, counters=False, cu_seqlens=cu_seqlens)
-        ctx.cache = cache
-        ctx.save_for_backward(cache.q, cache.k, cache.v, cache.log_rem, cache.first_kb, cache.M)
-        rem = torch.exp(log_rem)
-        ctx.mark_non_differentiable(log_rem)
-        return o, rem
+    """Autograd over the C ABI.  Only tensors go through save_for_backward (so
+    saved-tensor hooks such as CPU offload see all of them); ctx keeps scalars,
+    the layout and the host copy of cu_seqlens."""
 
     @staticmethod
-    def backward(ctx, d_o, d_rem):
-        q, k, v, log_rem, first_kb, M = ctx.saved_tensors
-        c = ctx.cache
-        cache = BlockedCache(q, k, v, c.scale, c.layout, log_rem, first_kb, M, c.skip, c.skip_eps,
-                             cu_seqlens=c.cu_seqlens, max_seqlen=c.max_seqlen, cu_host=c.cu_host)
+    def forward(ctx, q, k, v, scale, skip, skip_eps, cu_seqlens, return_rem):
+        o, log_rem, _, cache = blocked_forward(q, k, v, skip=skip, skip_eps=skip_eps,
+                                               scale=scale, counters=False, cu_seqlens=cu_seqlens)
+        ctx.set_materialize_grads(False)
+        ctx.meta = (cache.scale, cache.layout, cache.skip, cache.skip_eps, cache.max_seqlen,
+                    cache.cu_host, cache.cu_seqlens is not None)
+        extra = (cache.cu_seqlens,) if cache.cu_seqlens is not None else ()
+        ctx.save_for_backward(cache.q, cache.k, cache.v, log_rem, cache.first_kb, cache.M, *extra)
+        ctx.return_rem = return_rem
+        if return_rem:
+            return o, torch.exp(log_rem)
+        return o
+
+    @staticmethod
+    def backward(ctx, d_o, d_rem=None):
+        q, k, v, log_rem, first_kb, M, *extra = ctx.saved_tensors
+        scale, layout, skip, skip_eps, max_seqlen, cu_host, varlen = ctx.meta
+        cache = BlockedCache(q, k, v, scale, layout, log_rem, first_kb, M, skip, skip_eps,
+                             cu_seqlens=extra[0] if varlen else None, max_seqlen=max_seqlen,
+                             cu_host=cu_host)
+        if d_o is None and d_rem is None:
+            return None, None, None, None, None, None, None, None
         if d_o is None:
             d_o = torch.zeros_like(q)
         # rem_j = 1 - sum_i A_ij  =>  dL/dA_ij -= dL/drem_j : the reference's
         # row_offset hook (blocked.py:241-242, model.py:227-230)
         dq, dk, dv, _ = blocked_backward_twophase(cache, d_o.to(torch.bfloat16), row_offset=d_rem)
-        return dq, dk, dv, None, None, None, None
+        return dq, dk, dv, None, None, None, None, None
 
 
 def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool = False,
@@ -382,6 +441,10 @@ def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool =
     and is differentiable.  skip enables the reference's block skipping
     (exact: a skipped block's weights are below skip_eps).
 
+    Without autograd (torch.no_grad(), or no input requiring grad) the forward
+    writes no M snapshots (blocked_forward(two_phase=False)): same outputs, no
+    O(L^2/64) intermediate.
+
     Packed varlen: q, k, v (total_tokens, heads, head_dim) and cu_seqlens (int32
     [n_seq+1] offsets); each sequence attends only within itself.
     """
@@ -393,5 +456,10 @@ def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool =
         skip_eps = SKIP_EPS_BF16
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[-1])
-    o, rem = _StickBreakingFn.apply(q, k, v, float(scale), bool(skip), float(skip_eps), cu_seqlens)
-    return (o, rem) if return_rem else o
+    if not (torch.is_grad_enabled() and (q.requires_grad or k.requires_grad or v.requires_grad)):
+        o, log_rem, _, _ = blocked_forward(q, k, v, skip=bool(skip), skip_eps=float(skip_eps),
+                                           scale=float(scale), counters=False,
+                                           cu_seqlens=cu_seqlens, two_phase=False)
+        return (o, torch.exp(log_rem)) if return_rem else o
+    return _StickBreakingFn.apply(q, k, v, float(scale), bool(skip), float(skip_eps), cu_seqlens,
+                                  bool(return_rem))

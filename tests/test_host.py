@@ -48,3 +48,17 @@ def test_unit_ranges_partition(n, world):
         seen.extend(range(lo, hi))
         assert hi - lo in (n // world, n // world + 1)
     assert seen == list(range(n))
+
+
+def test_dense_layout_check():
+    """a fused-QKV slice is strided but not dense; it must be copied."""
+    import torch
+    from paper_2410_17980_b200.ops import _dense, _same_layout
+    x = torch.zeros(2, 5, 3, 4, 64)  # (B, L, 3, H, d)
+    assert _dense(x) and _dense(x.transpose(1, 3))
+    q = x[:, :, 0].transpose(1, 2)  # (B, H, L, d) view with stride 3*H*d over L
+    assert not _dense(q)
+    assert _same_layout(q, q, q)[0].is_contiguous()
+    blhd = torch.zeros(2, 5, 4, 64).transpose(1, 2)
+    assert _dense(blhd) and _same_layout(blhd, blhd, blhd)[0].stride() == blhd.stride()
+    assert _dense(torch.zeros(1, 1, 7, 64)[:, :, :, :])

@@ -126,3 +126,27 @@ def test_python_op_refuses_cpu_tensors():
     q = torch.zeros(1, 1, 8, 64, dtype=torch.bfloat16)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         sb.stickbreaking_attention(q, q, q)
+
+
+def test_skip_rejects_stop_index_overflow(lib):
+    """The skip-on forward packs a stop tile into 13 bits: nb >= 8192 is refused."""
+    p = _params(L=8192 * 64, skip=1)
+    d = ctypes.c_void_p(16)
+    assert lib.sb_fwd(ctypes.byref(p), d, d, d, d, d, d, d, None, None) == 4
+    p = _params(L=8191 * 64, skip=0)  # skip off has no such limit (no device call: d=96)
+    p.head_dim = 96
+    assert lib.sb_fwd(ctypes.byref(p), d, d, d, d, d, d, d, None, None) == 4
+
+
+def test_store_mode_needs_no_n_but_recompute_does(lib):
+    p = _params()
+    d = ctypes.c_void_p(16)
+    # recompute mode (no workspace) without N: NULL error before any device work
+    rc = lib.sb_bwd_ws(ctypes.byref(p), d, d, d, d, None, None, d, d, None, d, d, d, None, 0, 3,
+                       None)
+    assert rc == 5
+    # store mode with a workspace smaller than sb_bwd_tile_bytes: shape error
+    rc = lib.sb_bwd_ws(ctypes.byref(p), d, d, d, d, None, None, d, d, None, d, d, d,
+                       ctypes.c_void_p(256), 1024, 3, None)
+    assert rc == 1
+    assert lib.sb_bwd_tile_bytes(ctypes.byref(p), None) == 1 * 2 * 2 * 3 * 16384 + 256

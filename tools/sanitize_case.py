@@ -3,7 +3,7 @@
 compute-sanitizer (GPU only):
 
     for t in memcheck racecheck synccheck; do
-      compute-sanitizer --tool $t python tools/sanitize_case.py; done
+      compute-sanitizer --tool $t python tools/sanitize_case.py [--many]; done
 """
 import os
 import sys
@@ -14,7 +14,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2410_17980_b200 as sb  # noqa: E402
 from tests.gpu_util import make_qkv  # noqa: E402
 
-for (B, H, L, d, skip) in [(1, 2, 320, 128, False), (1, 2, 256, 64, True)]:
+CASES = [(1, 2, 320, 128, False), (1, 2, 256, 64, True)]
+if "--many" in sys.argv:
+    # >= 3 items per CTA in every kernel (512 forward / phase-1 items, 1024 phase-2
+    # items over 148 CTAs): the cross-item barrier phases and the work-queue ring wrap
+    CASES = [(4, 64, 512, 64, False), (4, 64, 512, 128, True)]
+for (B, H, L, d, skip) in CASES:
     q, k, v, do = make_qkv(B, H, L, d, seed=1)
     o, lr, st, cache = sb.blocked_forward(q, k, v, skip=skip)
     for store in (False, True):
