@@ -1123,7 +1123,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         constexpr int HD = D / 2;
         const int key0 = wi.kb0 * kBlock + quarter * 32;
         const int nvalid = max(0, min(32, u.L - key0));
-        const uint32_t stage = smem_u32(smem + C::kOffA) + (warp & 7) * (32 * HD * 2);
+        // the warp's OWN 32 A rows (4 KB at w * kPBytes + quarter * 4 KB): the other
+        // warpgroup may already be writing A rows of its next item (at D = 64 a
+        // packed 2 KB-per-warp staging overlapped them: racecheck, many items per CTA)
+        static_assert(32 * HD * 2 <= 32 * 128, "staging fits the warp's own A rows");
+        const uint32_t stage = smem_u32(smem + C::kOffA) + (warp & 7) * (32 * 128);
 #pragma unroll 1
         for (int t = 0; t < 2; ++t) {
           float a[HD];
@@ -1650,7 +1654,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         constexpr int HD = D / 2;
         const int key0 = wi.kb0 * kBlock + quarter * 32;
         const int nvalid = max(0, min(32, u.L - key0));
-        const uint32_t stage = smem_u32(smem + C::kOffA) + (warp & 7) * (32 * HD * 2);
+        // the warp's OWN 32 A rows (4 KB at w * kPBytes + quarter * 4 KB): the other
+        // warpgroup may already be writing A rows of its next item (at D = 64 a
+        // packed 2 KB-per-warp staging overlapped them: racecheck, many items per CTA)
+        static_assert(32 * HD * 2 <= 32 * 128, "staging fits the warp's own A rows");
+        const uint32_t stage = smem_u32(smem + C::kOffA) + (warp & 7) * (32 * 128);
 #pragma unroll 1
         for (int t = 0; t < 2; ++t) {
           float a[HD];

@@ -128,13 +128,14 @@ def test_many_items_per_cta_all_units(d, skip, family):
     _check_units(a, ref, rdq, rdk, rdv, idx, f"B{B} H{H} L{L} d{d} skip={skip}")
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("store", [True, False])
-def test_varlen_many_items(store):
+def test_varlen_many_items(store, d):
     """A packed batch with > 148 items per launch (40 sequences, 8 heads)."""
     import paper_2410_17980_b200 as sb
     rng = np.random.default_rng(5)
     lens = [int(x) for x in rng.integers(1, 1100, size=40)]
-    H, d = 8, 64
+    H = 8
     g = torch.Generator().manual_seed(9)
     T = sum(lens)
     q, k, v, d_o = (torch.randn(T, H, d, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
@@ -144,13 +145,15 @@ def test_varlen_many_items(store):
     o, log_rem, st, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu.cuda())
     dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, store_tiles=store)
     torch.cuda.synchronize()
-    worst = 0.0
+    worst = {}
     for b, Lb in enumerate(lens):
         s0, s1 = int(cu[b]), int(cu[b + 1])
         sl = [to64(t[s0:s1].transpose(0, 1)) for t in (q, k, v, d_o)]
         ref = oracle.tiled_forward(*sl[:3], block=64)
         rdq, rdk, rdv, _ = oracle.tiled_backward(*sl, ref, block=64)
-        for got, r in ((o, ref["o"]), (dq, rdq), (dk, rdk), (dv, rdv)):
-            worst = max(worst, rel_to_max(to64(got[s0:s1].transpose(0, 1)), r))
-    print("varlen many items: worst", worst)
-    assert worst < TOL
+        for n, got, r in (("o", o, ref["o"]), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+            e = rel_to_max(to64(got[s0:s1].transpose(0, 1)), r)
+            if e > worst.get(n, (0.0,))[0]:
+                worst[n] = (e, b, Lb)
+    print("varlen many items: worst (err, seq, L)", worst)
+    assert max(e for e, _, _ in worst.values()) < TOL, worst

@@ -6,6 +6,8 @@ the reference's own tolerances (test_blocked.py:71, :150, :203; 1e-10 / 1e-9
 in float64) and the float32 path must meet BASELINE.json's 1e-5 bound.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -123,3 +125,26 @@ def test_skip_soundness_random():
     on = oracle.tiled_forward(q, k, v, block=16, skip=True)
     assert np.max(np.abs(on["o"] - off["o"])) < 1e-9
     assert on["visited"] <= off["visited"]
+
+
+def test_c3_decision_generator_matches_c_oracle():
+    """tests/golden/gen_c3_first_kb.py (the C3 golden skip decisions) follows the C
+    oracle's blocked_forward decisions exactly on bf16 shifted-logit inputs."""
+    import importlib.util
+    import math
+    spec = importlib.util.spec_from_file_location(
+        "gen_c3", os.path.join(os.path.dirname(__file__), "golden", "gen_c3_first_kb.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    from tests.golden_inputs import bf16_round
+    rs = np.random.default_rng(4)
+    for mu in (-6.0, -7.0, 0.0):
+        L, d = 2048, 64
+        q = bf16_round(rs.standard_normal((L, d)))
+        k = bf16_round(rs.standard_normal((L, d)))
+        q[:, 0] = mu * math.sqrt(d)
+        k[:, 0] = 1.0
+        fkb, vis, m = gen.head_decisions(q, k)
+        ref = oracle.tiled_forward(q, k, np.zeros_like(q), block=64, skip=True, skip_eps=1e-6)
+        np.testing.assert_array_equal(fkb, ref["first_kb"])
+        assert vis == ref["visited"]

@@ -25,4 +25,14 @@ for (B, H, L, d, skip) in CASES:
     for store in (False, True):
         dq, dk, dv, _ = sb.blocked_backward_twophase(cache, do, store_tiles=store)
     torch.cuda.synchronize()
+if "--many" in sys.argv:  # packed varlen, > 148 items per launch, d = 64
+    g = torch.Generator().manual_seed(5)
+    lens = [int(x) for x in torch.randint(1, 1100, (40,), generator=g)]
+    T = sum(lens)
+    q, k, v, do = (torch.randn(T, 8, 64, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
+    cu = torch.tensor([0] + torch.tensor(lens).cumsum(0).tolist(), dtype=torch.int32).cuda()
+    o, lr, st, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu)
+    for store in (False, True):
+        dq, dk, dv, _ = sb.blocked_backward_twophase(cache, do, store_tiles=store)
+    torch.cuda.synchronize()
 print("sanitizer case ok")
