@@ -227,7 +227,7 @@ struct BwdQCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kVStages * kKVBytes;  // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8;
+  static constexpr int kNumBars = 2 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -287,8 +287,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int n_items = ((g.n_qt + 1) / 2) * g.B * g.H;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* bar_qdo = bars;
-  uint64_t* bar_kfull = bars + 1;
+  // Q/dO landed, one barrier per warpgroup (completes once per item with a tile for
+  // it; see the forward's bar_q: a shared one let WG1's issuer, skipping items
+  // without a second tile, alias a phase two ahead)
+  uint64_t* bar_qdo = bars;  // [2]
+  uint64_t* bar_kfull = bars + 2;
   uint64_t* bar_kempty = bar_kfull + ST;
   uint64_t* bar_vfull = bar_kempty + ST;
   uint64_t* bar_vempty = bar_vfull + VST;
@@ -300,6 +303,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qdo, 1);
+    mbar_init(bar_qdo + 1, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_kfull + s, 1);
       mbar_init(bar_kempty + s, 2);  // one arrival per warpgroup issuer (dQ read K)
@@ -350,15 +354,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         SB_TR(args, 0, ni, 12);
         if (leader) {
           const int nw = it.has1 ? 2 : 1;
-          mbar_expect_tx(bar_qdo, nw * 2 * C::kQBytes);
-          for (int w = 0; w < nw; ++w)
+          for (int w = 0; w < nw; ++w) {
+            mbar_expect_tx(bar_qdo + w, 2 * C::kQBytes);
             for (int c = 0; c < D / 64; ++c) {
               const int row0 = (2 * it.p + w) * kTileM;
-              tma_load_4d(&tm_q, bar_qdo, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
+              tma_load_4d(&tm_q, bar_qdo + w, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
                           c * 64, u.trow0 + row0, it.h, u.tb);
-              tma_load_4d(&tm_do, bar_qdo, smem + C::kOffDO + w * C::kQBytes + c * (kTileM * 128),
-                          c * 64, u.trow0 + row0, it.h, u.tb);
+              tma_load_4d(&tm_do, bar_qdo + w,
+                          smem + C::kOffDO + w * C::kQBytes + c * (kTileM * 128), c * 64,
+                          u.trow0 + row0, it.h, u.tb);
             }
+          }
         }
         __syncwarp();
         for (int j = 0; j < it.n_s; ++j, ++jg) {
@@ -441,7 +447,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           continue;
         }
         const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
-        mbar_wait(bar_qdo, ni & 1);
+        mbar_wait(bar_qdo + w, nwi & 1);  // this warpgroup's nwi-th tile
         // Static issue order: S(j+1) once S(j) was read (it runs while the
         // warpgroup still works on tile j), dQ(j) once dZ(j) is in smem, dW(j+1)
         // once dW(j) was read and V(j+1) landed (V is single-buffered).

@@ -35,7 +35,7 @@ struct FwdPPCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffP = kOffV + kStages * kKVBytes;       // P[wg][buf]
   static constexpr int kOffBar = kOffP + 4 * kPBytes;
-  static constexpr int kNumBars = 1 + 3 * kStages + 2 * 8 + 2 + 2 + 1 + 8 + 2 + 2;
+  static constexpr int kNumBars = 2 + 3 * kStages + 2 * 8 + 2 + 2 + 1 + 8 + 2 + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   // misc: TMEM slot, work-queue ring, skip flags (+64), skip max exchange (+128)
   static constexpr int kSmem = kOffMisc + 256 + 1024;
@@ -95,8 +95,13 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   const int n_items = ((g.n_qt + 1) / 2) * g.B * g.H;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* bar_q = bars;
-  uint64_t* bar_kfull = bars + 1;
+  // Q landed, one barrier per warpgroup: each completes once per item that has a
+  // tile for that warpgroup, so a warpgroup that sits out items (no second tile:
+  // odd tile counts, short varlen sequences) can never wait on a phase two ahead
+  // of the barrier (a parity wait cannot tell those apart: that race read a stale
+  // Q tile whenever WG1 skipped two items in a row)
+  uint64_t* bar_q = bars;  // [2]
+  uint64_t* bar_kfull = bars + 2;
   uint64_t* bar_vfull = bar_kfull + ST;
   uint64_t* bar_kvempty = bar_vfull + ST;
   uint64_t* wgbars = bar_kvempty + ST;  // per wg: sfull[2], sempty[2], pfull[2], pempty[2]
@@ -119,6 +124,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
+    mbar_init(bar_q + 1, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_kfull + s, 1);
       mbar_init(bar_vfull + s, 1);
@@ -167,11 +173,12 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const Unit& u = it.u;
       if (ni >= 1) mbar_wait(bar_qfree, (ni - 1) & 1);
       if (leader) {
-        mbar_expect_tx(bar_q, (it.has1 ? 2 : 1) * C::kQBytes);
-        for (int w = 0; w < (it.has1 ? 2 : 1); ++w)
+        for (int w = 0; w < (it.has1 ? 2 : 1); ++w) {
+          mbar_expect_tx(bar_q + w, C::kQBytes);
           for (int c = 0; c < D / 64; ++c)
-            tma_load_4d(&tm_q, bar_q, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
+            tma_load_4d(&tm_q, bar_q + w, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
                         c * 64, u.trow0 + (2 * it.p + w) * kTileM, it.h, u.tb);
+        }
       }
       __syncwarp();
       int n_load = it.n_s;
@@ -384,7 +391,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       {
         // copy this thread's Q row (TMA-swizzled smem) into TMEM lane r: the A
         // operand of S = Q K^T, two bf16 of d per 32-bit column
-        mbar_wait(bar_q, (ni - 1) & 1);
+        mbar_wait(bar_q + w, nwi & 1);  // this warpgroup's nwi-th tile
         const uint32_t qrow = smem_u32(smem + C::kOffQ + w * C::kQBytes) + r * 128;
         uint32_t qv[D / 2];
 #pragma unroll
