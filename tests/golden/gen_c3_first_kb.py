@@ -30,7 +30,9 @@ import sys
 import time
 from multiprocessing import Pool
 
-import numpy as np
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # before numpy: one BLAS thread per worker
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
@@ -104,7 +106,6 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 1)
     a = ap.parse_args()
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     import torch
     from tests.gpu_util import make_qkv
 
