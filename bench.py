@@ -223,39 +223,34 @@ def main():
                     for _ in range(4))
     stream = torch.cuda.current_stream()
 
-    # preallocated outputs so the timed region holds only our kernels
+    # preallocated outputs and workspace so the timed region holds only our kernels
     def step(ev=None):
         o, log_rem, _, cache = sb.blocked_forward(q, k, v, counters=False)
         if ev is not None:
             ev[1].record(stream)
-        out = step.out
-        sb.blocked_backward_twophase(cache, d_o, out=out, phases=1, tiles=step.tiles,
-                                     store_tiles=step.tiles is not None)
+        sb.blocked_backward_twophase(cache, d_o, out=step.out, phases=1, workspace=step.ws)
         if ev is not None:
             ev[2].record(stream)
-        sb.blocked_backward_twophase(cache, d_o, out=out, phases=2, tiles=step.tiles,
-                                     store_tiles=step.tiles is not None)
+        sb.blocked_backward_twophase(cache, d_o, out=step.out, phases=2, workspace=step.ws)
         return o
 
-    M_elems = sb.ops._lib.load().sb_snapshot_elems(
-        __import__("ctypes").byref(sb.ops._params(q, 1.0 / math.sqrt(D), False, 1e-6)))
-    # dZ tile workspace of the store-mode backward (shared by the two phase launches)
+    # the backward's transient workspace: M snapshots (phase 1 -> phase 2) + dZ tiles
     _, _, _, cache0 = sb.blocked_forward(q, k, v, counters=False)
-    n_tiles_bytes = sb.ops.tile_workspace_bytes(cache0)
-    step.tiles = (torch.empty(n_tiles_bytes, device=dev, dtype=torch.uint8)
-                  if n_tiles_bytes <= sb.ops.workspace_cap_bytes(dev) else None)
+    ws_bytes = sb.ops.workspace_bytes(cache0, store=True)
+    state_bytes = cache0.state.numel() * 4
     del cache0
-    # store mode needs no N snapshots (phase 2 reads dZ); recompute mode does
-    step.out = (None if step.tiles is not None else
-                torch.empty(M_elems, device=dev, dtype=torch.float32),
-                torch.empty_like(q), torch.empty_like(q), torch.empty_like(q))
-    snap_bytes = M_elems * 4
+    step.ws = torch.empty(ws_bytes, device=dev, dtype=torch.uint8)
+    step.out = tuple(torch.empty_like(q) for _ in range(3))
+    M_bytes = sb.ops._lib.load().sb_snapshot_elems(
+        __import__("ctypes").byref(sb.ops._params(q, 1.0 / math.sqrt(D), False, 1e-6))) * 4
     intermediates = {
-        "M_bytes": snap_bytes, "N_bytes": 0 if step.tiles is not None else snap_bytes,
-        "dZ_workspace_bytes": n_tiles_bytes if step.tiles is not None else 0,
-        "note": "per step: M written by the forward and read by both backward phases; N only "
-                "in recompute mode; the store-mode dZ workspace is written by phase 1 and read "
-                "by phase 2 (bf16, O(L^2)); an inference forward (no autograd) writes no M"}
+        "saved_state_bytes": state_bytes, "M_bytes": M_bytes, "N_bytes": 0,
+        "dZ_workspace_bytes": ws_bytes - M_bytes, "workspace_bytes": ws_bytes,
+        "note": "forward -> backward: only the O(L) state (final a per row, float64) plus "
+                "first_kb; the M snapshots are rolled back by phase 1 and live in the "
+                "backward's transient workspace with the store mode's dZ tiles (bf16, O(L^2), "
+                "written by phase 1, read by phase 2); no N; an inference forward (no autograd) "
+                "writes no state"}
 
     for _ in range(W):
         step()
@@ -296,8 +291,8 @@ def main():
     alg_flops = 7 * G  # fwd 2G + bwd 5G (FA convention)
     # executed: fwd 2G (QK^T, AV) + phase 1 3G (QK^T, dO V^T, dZ K) + phase 2: store mode
     # 3G (QK^T, A^T dO, dZ^T Q; dZ read from phase 1's tiles), recompute mode 4G
-    store = step.tiles is not None
-    p2_exec = 3 * G if store else 4 * G
+    store = True
+    p2_exec = 3 * G
     exec_flops = 5 * G + p2_exec
     tflops = world * alg_flops * K / (total_ms / 1e3) / 1e12
     burst, sustained, peak_kind = load_peaks()
@@ -308,7 +303,7 @@ def main():
             and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"] and "sw_power_cap" not in clk["reasons"])
     peak = burst if held else sustained
     kernels = {"sb_fwd_pp_kernel": (fwd_ms, 2 * G, 2 * G), "sb_bwd_q_kernel": (p1_ms, 3 * G, 3 * G),
-               ("sb_bwd_kvs_kernel" if store else "sb_bwd_kv_kernel"): (p2_ms, 2 * G, p2_exec)}
+               "sb_bwd_kvs_kernel": (p2_ms, 2 * G, p2_exec)}
     dom = max(kernels, key=lambda n: kernels[n][0])
     d_ms, d_alg, d_exec = kernels[dom]
     achieved = d_alg / (d_ms / 1e3) / 1e12
@@ -456,8 +451,8 @@ def main():
                    "head_dim": D, "global_batch": B * world,
                    "parallelism": f"(b,h) units sharded, {world} independent ranks, no collective",
                    "l2": "inputs (4 x 128 MiB bf16 per rank) exceed the 126 MB L2; no flush",
-                   "backward": ("store mode (phase 1 writes dZ tiles, %.2f GB workspace)"
-                                % (step.tiles.numel() / 1e9) if store else "recompute mode")},
+                   "backward": "store mode (phase 1 writes dZ tiles, %.2f GB workspace)"
+                            % (ws_bytes / 1e9)},
         "tflops": tflops, "tflops_note": "algorithmic 7*B*H*L^2*d per step (FA causal convention)",
         "executed_tflops": world * exec_flops * K / (total_ms / 1e3) / 1e12,
         "ms": {"fwd": fwd_ms, "bwd_phase1": p1_ms, "bwd_phase2": p2_ms},

@@ -10,18 +10,30 @@
  * Reference interfaces each entry point replaces (paths under
  * /root/reference/pkg/src/sbattn/):
  *   sb_fwd       blocked.py:129  blocked_forward(q, k, v, layout, skip, skip_eps,
- *                                two_phase=True)  -> (o, RowLogAccumulator, TileStats)
+ *                                two_phase)      -> (o, RowLogAccumulator, TileStats)
  *                blocked.py:218  sb_forward_blocked(q, k, v, layout, **kw)
  *   sb_bwd       blocked.py:299  blocked_backward_twophase(cache, d_o, layout,
  *                                row_offset)     -> (d_q, d_k, d_v, n_stored)
- *   sb_bwd_phase blocked.py:337-357 / :367-386, the two phases of sb_bwd
- *   sb_bwd_ws    sb_bwd_phase with the dZ tile workspace (store mode: phase 2 reads
- *                phase 1's dZ instead of recomputing it; same results)
- *   sb_snapshot_elems  blocked.py:58-60 BlockLayout.n_tiles x d_block (M/N size)
- *   sb_varlen_elems    the same sizes for a packed variable-length batch (each
- *                      sequence planned separately)
- *   sb_status_string   the ValueError messages of blocked.py:115-119, :155-156,
- *                      :246-247, :315-316, :398-399
+ *                (phases = 1 / 2: its two sweeps, blocked.py:337-357 / :367-386)
+ *   sb_state_elems          the BlockedCache (blocked.py:90-98) the backward needs
+ *                           beyond q, k, v and first_kb: O(L) per head here
+ *   sb_bwd_workspace_bytes  the M / N snapshot dicts (RowLogAccumulator.m_blocks,
+ *                           blocked.py:70-80, :353) + the dZ tile store, all
+ *                           transient inside one backward call
+ *   sb_snapshot_elems / sb_varlen_elems  blocked.py:58-60 BlockLayout.n_tiles x
+ *                           d_block (one snapshot array), first_kb sizes for varlen
+ *   sb_status_string        the ValueError messages of blocked.py:115-119,
+ *                           :155-156, :246-247, :315-316, :398-399
+ *
+ * Intermediates (BASELINE north_star: "cut the O(L^2/d_block) M/N intermediates"):
+ * the reference keeps one `a` snapshot per row per visited tile from the forward
+ * to the backward (M, blocked.py:188-189) and one `b` snapshot per row per tile
+ * between its two backward sweeps (N, :353).  Here the forward keeps only the
+ * final `a` per row (float64, the `state` array: O(L)); phase 1 of the backward
+ * rolls the per-tile snapshots back from it (M(kb) = a_final + the row totals of
+ * -lt of tiles <= kb, recomputed from the same tile math) and hands them to
+ * phase 2 inside the caller's workspace.  The store-mode backward has no N at
+ * all (phase 2 reads phase 1's dZ tiles).
  */
 #ifndef SB_ATTN_H
 #define SB_ATTN_H
@@ -40,7 +52,7 @@ enum {
   SB_ERR_SKIP_EPS = 2,     /* skip_eps outside (0, 1) (blocked.py:155-156) */
   SB_ERR_BLOCK = 3,        /* d_block != 64 or seq_len < 1 (blocked.py:64-65) */
   SB_ERR_UNSUPPORTED = 4,  /* head_dim not in {64, 128}, non-16B-aligned strides */
-  SB_ERR_NULL = 5,         /* required pointer is NULL (e.g. missing M, blocked.py:315-316) */
+  SB_ERR_NULL = 5,         /* required pointer is NULL (e.g. missing state, blocked.py:315-316) */
   SB_ERR_DEVICE = 6,       /* no sm_100 device / driver entry point unavailable */
   SB_ERR_LAUNCH = 7        /* CUDA launch or tensor-map encoding failed */
 };
@@ -69,63 +81,58 @@ typedef struct sb_params {
   int32_t total_tokens;      /* varlen only: rows of the packed tensors */
 } sb_params_t;
 
-/* Number of float elements of ONE snapshot array (M or N):
- * batch * heads * n_tiles * 64 with n_tiles = nb*(nb+1)/2, nb = ceil(L/64). */
+/* Float elements of ONE snapshot array (M or N) of a uniform batch: 64 (header)
+ * + batch * heads * n_tiles * 64 with n_tiles = nb*(nb+1)/2, nb = ceil(L/64);
+ * 0 for varlen batches (use sb_varlen_elems). */
 size_t sb_snapshot_elems(const sb_params_t* p);
 
+/* Float elements of the forward's state array (the only O(L)-sized thing the
+ * backward needs from the forward besides first_kb): 64 + 2 * rows (the final
+ * a of every row as float64), rows = batch*heads*seqlen, or total_tokens*heads
+ * for varlen.  16-byte aligned. */
+size_t sb_state_elems(const sb_params_t* p);
+
 /* Varlen sizes from a HOST copy of cu_seqlens ([batch+1]): *snapshot = floats of
- * one M/N array (heads * sum_b n_tiles(L_b) * 64), *first_kb = int32 elements
- * of first_kb (heads * sum_b nb(L_b)).  Returns SB_OK or SB_ERR_SHAPE
+ * one snapshot array (64 + heads * sum_b n_tiles(L_b) * 64), *first_kb = int32
+ * elements of first_kb (heads * sum_b nb(L_b)).  Returns SB_OK or SB_ERR_SHAPE
  * (decreasing offsets). */
 int sb_varlen_elems(const sb_params_t* p, const int32_t* cu_seqlens_host, size_t* snapshot,
                     size_t* first_kb);
 
 /* Forward.  Outputs: o (bf16, q's layout), log_rem [B,H,L] float (natural log of
  * the remaining stick mass, RowLogAccumulator.a), first_kb [B,H,nb] int32
- * (TileStats.first_kb), M (snapshot array, opaque; required by sb_bwd),
+ * (TileStats.first_kb), state (sb_state_elems floats, opaque; required by sb_bwd),
  * tile_counters (nullable) += {visited} (TileStats.visited).  stream is a
  * cudaStream_t (NULL = legacy default stream).
- * M may be NULL: a forward for inference that writes no snapshots, the
- * reference's blocked_forward(two_phase=False) (blocked.py:136, :163, :188);
- * results are identical, only sb_bwd cannot follow it. */
+ * state may be NULL: a forward for inference, the reference's
+ * blocked_forward(two_phase=False) (blocked.py:136, :163, :188); o, log_rem and
+ * first_kb are identical, only sb_bwd cannot follow it.  No call writes anything
+ * O(L^2/64) sized. */
 int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, void* o,
-           float* log_rem, int32_t* first_kb, float* M, unsigned long long* tile_counters,
+           float* log_rem, int32_t* first_kb, float* state, unsigned long long* tile_counters,
            void* stream);
 
-/* Two-phase backward.  row_offset (nullable) [B,H,L] float is the per-row
- * offset subtracted from dO.V^T (blocked.py:241-242, :274-276); N is a
- * caller-provided snapshot workspace (sb_snapshot_elems floats).  Writes dq,
- * dk, dv (bf16, q's layout).  log_rem is unused (the backward reads the per-tile
- * M snapshots) and may be NULL. */
+/* Bytes of the backward's workspace: the M snapshots (+ header), then either
+ * (store != 0) the dZ tiles phase 1 writes for phase 2 (bf16, 16 KB per 128-row x
+ * 64-key tile, n_qt*(n_qt+1) per (b,h) unit, n_qt = ceil(L/128)) or (store == 0,
+ * recompute mode: phase 2 recomputes dO.V^T and dZ) the N snapshots.  Same
+ * results bit for bit either way.  cu_seqlens_host: host offsets for varlen
+ * batches (else NULL).  0 if the sizes cannot be computed. */
+size_t sb_bwd_workspace_bytes(const sb_params_t* p, const int32_t* cu_seqlens_host, int store);
+
+/* Two-phase backward.  row_offset (nullable) [B,H,L] float is the per-row offset
+ * subtracted from dO.V^T (blocked.py:241-242, :274-276); state and first_kb come
+ * from sb_fwd on the same inputs (sb_bwd reads only the per-row part past the
+ * 64-float header).  workspace: device, 128-byte aligned, at least
+ * sb_bwd_workspace_bytes(p, cu_seqlens_host, store) bytes (checked: SB_ERR_SHAPE;
+ * varlen batches must pass cu_seqlens_host).  phases = 3 runs both sweeps; 1 runs
+ * phase 1 (dq, the M snapshots and the dZ tiles or N, blocked.py:337-357); 2 runs
+ * phase 2 (dk, dv, blocked.py:367-386) and must follow phase 1 on the stream with
+ * the same workspace.  Writes dq, dk, dv (bf16, q's layout). */
 int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
-           const float* row_offset, const float* log_rem, const int32_t* first_kb,
-           const float* M, float* N, void* dq, void* dk, void* dv, void* stream);
-
-/* The two kernels of sb_bwd, separately: phases = 1 runs phase 1 (dq and N,
- * blocked.py:337-357), 2 runs phase 2 (dk, dv from N, blocked.py:367-386),
- * 3 runs both (== sb_bwd).  Phase 2 must follow phase 1 on the stream. */
-int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void* v,
-                 const void* d_o, const float* row_offset, const float* log_rem,
-                 const int32_t* first_kb, const float* M, float* N, void* dq, void* dk, void* dv,
-                 int phases, void* stream);
-
-/* Store mode of the backward.  Bytes of the dZ tile workspace: phase 1 writes
- * every 128-row x 64-key dZ tile it computes (bf16, 16 KB each; per (b,h) unit
- * n_qt*(n_qt+1) tiles, n_qt = ceil(L/128)) and phase 2 reads them back instead of
- * recomputing dO.V^T and dZ (same results, bit for bit), plus 256 bytes of
- * work-queue counters.  cu_seqlens_host: host copy of the offsets for packed
- * varlen batches, else NULL. */
-size_t sb_bwd_tile_bytes(const sb_params_t* p, const int32_t* cu_seqlens_host);
-
-/* sb_bwd_phase with an optional dZ tile workspace (ztiles: device, 128-byte
- * aligned, ztiles_bytes >= sb_bwd_tile_bytes; NULL = recompute mode).  In store
- * mode N may be NULL (phase 2 reads dZ, not the b snapshots) and is not written.
- * Uniform batches get SB_ERR_SHAPE for a short workspace; for varlen batches
- * the caller must size it with sb_bwd_tile_bytes(p, cu_seqlens_host). */
-int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
-              const float* row_offset, const float* log_rem, const int32_t* first_kb,
-              const float* M, float* N, void* dq, void* dk, void* dv, void* ztiles,
-              size_t ztiles_bytes, int phases, void* stream);
+           const float* row_offset, const float* state, const int32_t* first_kb, void* dq,
+           void* dk, void* dv, void* workspace, size_t workspace_bytes,
+           const int32_t* cu_seqlens_host, int store, int phases, void* stream);
 
 const char* sb_status_string(int status);
 int sb_version(void);

@@ -28,8 +28,8 @@ class SbParams(ctypes.Structure):
     ]
 
 
-EXPORTS = ("sb_fwd", "sb_bwd", "sb_bwd_phase", "sb_bwd_ws", "sb_bwd_tile_bytes",
-           "sb_snapshot_elems", "sb_varlen_elems", "sb_status_string", "sb_version")
+EXPORTS = ("sb_fwd", "sb_bwd", "sb_bwd_workspace_bytes", "sb_state_elems", "sb_snapshot_elems",
+           "sb_varlen_elems", "sb_status_string", "sb_version")
 
 _lib = None
 
@@ -55,17 +55,15 @@ def load(path: str = LIB_PATH):
     lib.sb_varlen_elems.restype = ctypes.c_int
     lib.sb_varlen_elems.argtypes = [PP, P, ctypes.POINTER(ctypes.c_size_t),
                                     ctypes.POINTER(ctypes.c_size_t)]
+    lib.sb_state_elems.restype = ctypes.c_size_t
+    lib.sb_state_elems.argtypes = [PP]
     lib.sb_fwd.restype = ctypes.c_int
     lib.sb_fwd.argtypes = [PP, P, P, P, P, P, P, P, P, P]
+    lib.sb_bwd_workspace_bytes.restype = ctypes.c_size_t
+    lib.sb_bwd_workspace_bytes.argtypes = [PP, P, ctypes.c_int]
     lib.sb_bwd.restype = ctypes.c_int
-    lib.sb_bwd.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, P, P]
-    lib.sb_bwd_phase.restype = ctypes.c_int
-    lib.sb_bwd_phase.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_int, P]
-    lib.sb_bwd_ws.restype = ctypes.c_int
-    lib.sb_bwd_ws.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_size_t,
-                              ctypes.c_int, P]
-    lib.sb_bwd_tile_bytes.restype = ctypes.c_size_t
-    lib.sb_bwd_tile_bytes.argtypes = [PP, P]
+    lib.sb_bwd.argtypes = [PP, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_size_t, P,
+                           ctypes.c_int, ctypes.c_int, P]
     lib.sb_status_string.restype = ctypes.c_char_p
     lib.sb_status_string.argtypes = [ctypes.c_int]
     lib.sb_version.restype = ctypes.c_int

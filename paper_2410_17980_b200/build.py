@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsbattn.so")
-SOURCES = ["sb_api.cu", "sb_fwd.cu", "sb_fwd_pp.cu", "sb_bwd.cu"]
+SOURCES = ["sb_api.cu", "sb_fwd_pp.cu", "sb_bwd.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

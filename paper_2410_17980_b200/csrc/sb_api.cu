@@ -120,41 +120,84 @@ bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15)
 
 uint32_t* g_trace = nullptr;  // SB_TRACE builds: set by sb_debug_set_trace
 
+// Snapshot floats (header + one float per row per tile) of a uniform batch or, with
+// host offsets, of a packed varlen batch; -1 on bad offsets.
+int64_t snapshot_floats(const sb_params_t* p, const int32_t* cu_host) {
+  if (!p->cu_seqlens) {
+    const int64_t nb = (p->seqlen + 63) / 64;
+    return sb::kSchedHeader + (int64_t)p->batch * p->heads * (nb * (nb + 1) / 2) * 64;
+  }
+  if (!cu_host) return -1;
+  int64_t tiles = 0;
+  for (int b = 0; b < p->batch; ++b) {
+    const int64_t L = cu_host[b + 1] - cu_host[b];
+    if (L < 0) return -1;
+    const int64_t nb = (L + 63) / 64;
+    tiles += nb * (nb + 1) / 2;
+  }
+  return sb::kSchedHeader + (int64_t)p->heads * tiles * 64;
+}
+
+// dZ tiles (store mode) of a uniform or (host offsets) varlen batch; -1 on bad offsets.
+int64_t ztile_count(const sb_params_t* p, const int32_t* cu_host) {
+  if (!p->cu_seqlens) {
+    const int64_t nq = (p->seqlen + 127) / 128;
+    return (int64_t)p->batch * p->heads * nq * (nq + 1);
+  }
+  if (!cu_host) return -1;
+  int64_t tiles = 0;
+  for (int b = 0; b < p->batch; ++b) {
+    const int64_t nq = (cu_host[b + 1] - cu_host[b] + 127) / 128;
+    tiles += (int64_t)p->heads * nq * (nq + 1);
+  }
+  return tiles;
+}
+
+constexpr int64_t kWsAlign = 1024;
+int64_t round_up(int64_t x) { return (x + kWsAlign - 1) / kWsAlign * kWsAlign; }
+
 }  // namespace
 
 extern "C" {
 
 size_t sb_snapshot_elems(const sb_params_t* p) {
+  if (!p || p->seqlen < 1 || p->cu_seqlens) return 0;
+  return (size_t)snapshot_floats(p, nullptr);
+}
+
+size_t sb_state_elems(const sb_params_t* p) {
   if (!p || p->seqlen < 1) return 0;
-  const size_t nb = (size_t)(p->seqlen + 63) / 64;
-  return sb::kSchedHeader + (size_t)p->batch * p->heads * (nb * (nb + 1) / 2) * 64;
+  const int64_t rows = p->cu_seqlens ? (int64_t)p->total_tokens * p->heads
+                                     : (int64_t)p->batch * p->heads * p->seqlen;
+  return (size_t)(sb::kSchedHeader + 2 * rows);
 }
 
 int sb_varlen_elems(const sb_params_t* p, const int32_t* cu, size_t* snapshot,
                     size_t* first_kb) {
   if (!p || !cu || !snapshot || !first_kb) return SB_ERR_NULL;
-  size_t tiles = 0, nbs = 0;
+  size_t nbs = 0;
   for (int b = 0; b < p->batch; ++b) {
     const int L = cu[b + 1] - cu[b];
     if (L < 0) return SB_ERR_SHAPE;
-    const size_t nb = (size_t)(L + 63) / 64;
-    tiles += nb * (nb + 1) / 2;
-    nbs += nb;
+    nbs += (size_t)(L + 63) / 64;
   }
-  *snapshot = sb::kSchedHeader + (size_t)p->heads * tiles * 64;
+  sb_params_t q = *p;
+  q.cu_seqlens = cu;  // any non-NULL: varlen sizing from the host offsets
+  *snapshot = (size_t)snapshot_floats(&q, cu);
   *first_kb = (size_t)p->heads * nbs;
   return SB_OK;
 }
 
 int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, void* o,
-           float* log_rem, int32_t* first_kb, float* M, unsigned long long* tile_counters,
+           float* log_rem, int32_t* first_kb, float* state, unsigned long long* tile_counters,
            void* stream) {
   int st = validate(p);
   if (st) return st;
-  // M == NULL: forward for inference, no snapshots (blocked_forward(two_phase=False),
+  // state == NULL: forward for inference (blocked_forward(two_phase=False),
   // blocked.py:136, :163, :188); the backward then cannot run on this forward
   if (!q || !k || !v || !o || !log_rem || !first_kb) return SB_ERR_NULL;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return SB_ERR_UNSUPPORTED;
+  if (state && !aligned16(state)) return SB_ERR_UNSUPPORTED;
   CUtensorMap tq, tk, tv;
   if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tk, k, p, 64)) ||
       (st = make_map(&tv, v, p, 64)))
@@ -164,86 +207,51 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   a.o = reinterpret_cast<__nv_bfloat16*>(o);
   a.log_rem = log_rem;
   a.first_kb = first_kb;
-  a.M = M;
+  a.state = state ? reinterpret_cast<double*>(state + sb::kSchedHeader) : nullptr;
   a.counters = tile_counters;
   const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
   a.log_eps = std::log(eps);
   a.trace = g_trace;
-  a.sched = reinterpret_cast<unsigned*>(M);  // NULL: items dealt statically
-  // the persistent ping-pong product-form kernel, with the exact skip decisions
-  // when skip is on; SB_FWD_SKIP_V1=1 selects the older all-log-space skip kernel
-  // (sb_fwd.cu, kept as a cross-check)
-  cudaStream_t st_ = reinterpret_cast<cudaStream_t>(stream);
-  static const bool v1 = [] {
-    const char* e = std::getenv("SB_FWD_SKIP_V1");
-    return e && e[0] == '1';
-  }();
-  int rc = (p->skip && v1 && M) ? sb::fwd_dispatch(p->head_dim, true, tq, tk, tv, a, st_)
-                           : sb::fwd_pp_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a, st_);
+  a.sched = reinterpret_cast<unsigned*>(state);  // NULL: items dealt statically
+  int rc = sb::fwd_pp_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a,
+                               reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
 
-int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
-           const float* row_offset, const float* log_rem, const int32_t* first_kb,
-           const float* M, float* N, void* dq, void* dk, void* dv, void* stream) {
-  return sb_bwd_phase(p, q, k, v, d_o, row_offset, log_rem, first_kb, M, N, dq, dk, dv, 3, stream);
-}
-
-size_t sb_bwd_tile_bytes(const sb_params_t* p, const int32_t* cu) {
+size_t sb_bwd_workspace_bytes(const sb_params_t* p, const int32_t* cu_host, int store) {
   if (!p || p->seqlen < 1) return 0;
-  size_t tiles = 0;
-  if (!p->cu_seqlens) {
-    const size_t nq = (size_t)(p->seqlen + 127) / 128;
-    tiles = (size_t)p->batch * p->heads * nq * (nq + 1);
-  } else {
-    if (!cu) return 0;
-    for (int b = 0; b < p->batch; ++b) {
-      const size_t nq = (size_t)(cu[b + 1] - cu[b] + 127) / 128;
-      tiles += (size_t)p->heads * nq * (nq + 1);
-    }
-  }
-  // + the backward's work-queue counters after the last tile (store mode needs no N)
-  return tiles * sb::kZTileBytes + sb::kZTailBytes;
+  const int64_t m = snapshot_floats(p, cu_host), z = ztile_count(p, cu_host);
+  if (m < 0 || z < 0) return 0;
+  const int64_t mb = round_up(m * 4);
+  return (size_t)(store ? mb + z * sb::kZTileBytes : mb + m * 4);
 }
 
-int sb_bwd_phase(const sb_params_t* p, const void* q, const void* k, const void* v,
-                 const void* d_o, const float* row_offset, const float* log_rem,
-                 const int32_t* first_kb, const float* M, float* N, void* dq, void* dk, void* dv,
-                 int phases, void* stream) {
-  return sb_bwd_ws(p, q, k, v, d_o, row_offset, log_rem, first_kb, M, N, dq, dk, dv, nullptr, 0,
-                   phases, stream);
-}
-
-int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
-              const float* row_offset, const float* log_rem, const int32_t* first_kb,
-              const float* M, float* N, void* dq, void* dk, void* dv, void* ztiles,
-              size_t ztiles_bytes, int phases, void* stream) {
+int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, const void* d_o,
+           const float* row_offset, const float* state, const int32_t* first_kb, void* dq,
+           void* dk, void* dv, void* workspace, size_t workspace_bytes,
+           const int32_t* cu_seqlens_host, int store, int phases, void* stream) {
   if (phases < 1 || phases > 3) return SB_ERR_SHAPE;
   int st = validate(p);
   if (st) return st;
-  (void)log_rem;  // unused (may be NULL): the backward reads the per-tile M snapshots
-  const bool store = ztiles != nullptr;
-  // N (the b snapshots) is read only by the recompute-mode phase 2: store mode takes
-  // dZ from the tile workspace instead and needs no N
-  if (!q || !k || !v || !d_o || !first_kb || !dq || !dk || !dv || (!N && !store))
-    return SB_ERR_NULL;
-  if (!M) return SB_ERR_NULL;  // blocked.py:315-316: M snapshots missing
+  if (!q || !k || !v || !d_o || !first_kb || !dq || !dk || !dv || !workspace) return SB_ERR_NULL;
+  if (!state) return SB_ERR_NULL;  // blocked.py:315-316: the forward's state is missing
+  if (p->cu_seqlens && !cu_seqlens_host) return SB_ERR_NULL;  // varlen sizes need the offsets
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(d_o) || !aligned16(dq) ||
-      !aligned16(dk) || !aligned16(dv))
+      !aligned16(dk) || !aligned16(dv) || !aligned16(state) ||
+      (reinterpret_cast<uintptr_t>(workspace) & 127))
     return SB_ERR_UNSUPPORTED;
-  if (store) {
-    // uniform batches are checked here; a varlen caller sizes the workspace with
-    // sb_bwd_tile_bytes(p, host cu_seqlens) (the device offsets are not read here)
-    if (ztiles_bytes < sb::kZTailBytes + sb::kZTileBytes) return SB_ERR_SHAPE;
-    if (!p->cu_seqlens && ztiles_bytes < sb_bwd_tile_bytes(p, nullptr)) return SB_ERR_SHAPE;
-    if (reinterpret_cast<uintptr_t>(ztiles) & 127) return SB_ERR_UNSUPPORTED;
-  }
+  const size_t need = sb_bwd_workspace_bytes(p, cu_seqlens_host, store);
+  if (need == 0 || workspace_bytes < need) return SB_ERR_SHAPE;
+  const int64_t m = snapshot_floats(p, cu_seqlens_host), mb = round_up(m * 4);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   CUtensorMap tq, tdo, tk, tv, tz;
   if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
       (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)))
     return st;
   std::memset(&tz, 0, sizeof(tz));
-  if (store && (st = make_tile_map(&tz, ztiles, ztiles_bytes - sb::kZTailBytes))) return st;
+  if (store && (st = make_tile_map(&tz, ws + mb, (size_t)ztile_count(p, cu_seqlens_host) *
+                                                   sb::kZTileBytes)))
+    return st;
   sb::BwdArgs a;
   a.g = geom(p);
   a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
@@ -251,15 +259,16 @@ int sb_bwd_ws(const sb_params_t* p, const void* q, const void* k, const void* v,
   a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   a.row_offset = row_offset;
   a.first_kb = first_kb;
-  a.M = M;
-  a.N = N;
+  a.state = reinterpret_cast<const double*>(state + sb::kSchedHeader);
+  // workspace: M snapshots (written by phase 1; their header holds the work-queue
+  // counters), then the dZ tiles (store mode) or the N snapshots (recompute mode)
+  a.M = reinterpret_cast<float*>(ws);
+  a.N = store ? nullptr : reinterpret_cast<float*>(ws + mb);
+  a.q = reinterpret_cast<const __nv_bfloat16*>(q);
+  a.k = reinterpret_cast<const __nv_bfloat16*>(k);
   a.trace = g_trace;
-  // work-queue counters: the N header, or (store mode) the workspace's tail
-  a.sched = store ? reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(ztiles) + ztiles_bytes -
-                                                sb::kZTailBytes)
-                  : reinterpret_cast<unsigned*>(N);
-  if (store) a.N = nullptr;
-  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, a, phases, store,
+  a.sched = reinterpret_cast<unsigned*>(ws);
+  int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, a, phases, store != 0,
                             reinterpret_cast<cudaStream_t>(stream));
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
@@ -272,15 +281,18 @@ const char* sb_status_string(int s) {
     case SB_ERR_BLOCK: return "seq_len, batch, heads must be >= 1 and d_block must be 64";
     case SB_ERR_UNSUPPORTED: return "unsupported configuration (head_dim must be 64 or 128, "
                                     "16-byte aligned rows and strides)";
-    case SB_ERR_NULL: return "required pointer is NULL (two-phase backward needs M snapshots)";
+    case SB_ERR_NULL: return "required pointer is NULL (the two-phase backward needs the forward's "
+                             "state; varlen needs host cu_seqlens)";
     case SB_ERR_DEVICE: return "CUDA driver entry point unavailable (no sm_100 device?)";
     case SB_ERR_LAUNCH: return "CUDA launch failed";
     default: return "unknown status";
   }
 }
 
-int sb_version(void) { return 4; }  // 2: packed varlen; 3: dZ tile workspace (sb_bwd_ws);
-                                    // 4: M-free forward, N-free store mode
+int sb_version(void) { return 5; }  // 2: packed varlen; 3: dZ tile workspace (sb_bwd_ws);
+                                    // 4: M-free inference forward, N-free store mode;
+                                    // 5: O(L) forward state, M rolled back in phase 1,
+                                    //    one sb_bwd with a caller-sized workspace
 
 #ifdef SB_TRACE
 // debug builds only: device buffer of kTraceCtas*4*64*16 uint32 clock stamps

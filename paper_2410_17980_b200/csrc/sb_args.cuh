@@ -1,4 +1,4 @@
-// Kernel argument blocks shared by the launchers (sb_fwd.cu, sb_bwd.cu) and the C ABI.
+// Kernel argument blocks shared by the launchers (sb_fwd_pp.cu, sb_bwd.cu) and the C ABI.
 #pragma once
 #include "sb_common.cuh"
 
@@ -9,11 +9,12 @@ struct FwdArgs {
   __nv_bfloat16* o;
   float* log_rem;        // [B,H,L] natural log of remaining stick mass
   int32_t* first_kb;     // [B,H,nb]
-  float* M;              // [B,H,n_tiles,64] a-snapshots (log2 units), nullable
+  double* state;         // [B,H,L] final a per row (log2 units, float64): the O(L) state
+                         // the backward rolls the M snapshots back from; nullable
   unsigned long long* counters;  // [2]: visited tiles, total tiles (nullable)
   double log_eps;        // log(skip_eps)
   uint32_t* trace;       // SB_TRACE builds only (libsbattn_trace.so); null otherwise
-  unsigned* sched;       // work-queue counter (M header), zeroed before the launch
+  unsigned* sched;       // work-queue counter (state header), zeroed before the launch
 };
 
 struct BwdArgs {
@@ -23,10 +24,13 @@ struct BwdArgs {
   __nv_bfloat16* dv;
   const float* row_offset;  // [B,H,L] or null
   const int32_t* first_kb;  // [B,H,nb] from the forward
-  const float* M;           // forward snapshots (log2 units)
-  float* N;                 // phase-1 b snapshots, read by phase 2
+  const double* state;      // [B,H,L] the forward's final a per row (log2 units)
+  float* M;                 // a-snapshots (log2 units): phase 1 writes, phase 2 reads
+  float* N;                 // phase-1 b snapshots, read by the recompute-mode phase 2
+  const __nv_bfloat16* q;   // raw q / k rows: phase 1's rare exact lt path (a logit with
+  const __nv_bfloat16* k;   // 2^z = inf needs z itself)
   uint32_t* trace;          // SB_TRACE builds only (libsbattn_trace.so); null otherwise
-  unsigned* sched;          // work-queue counters [2] (N header), zeroed before the launch
+  unsigned* sched;          // work-queue counters [2] (M header), zeroed before the launch
 };
 
 // Event timeline for kernel tuning (tools/trace_kernels.py).  Compiled only with
@@ -48,7 +52,5 @@ int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUt
                  bool store, cudaStream_t stream);
 int fwd_pp_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
-int fwd_dispatch(int D, bool skip, const CUtensorMap& tq, const CUtensorMap& tk,
-                 const CUtensorMap& tv, const FwdArgs& a, cudaStream_t stream);
 
 }  // namespace sb

@@ -55,19 +55,19 @@ static_assert(128 * kRegsLowQ + 256 * kRegsHighQ <= kBwdThreads * kRegsLaunch, "
 // scheduler can interleave them: 6 FP32 ops + 1 ex2 per element.  A row whose
 // group product reaches 2^64 (large logits; t = inf included) falls back to one
 // rcp per element.
+// Split in two so phase 1 can derive E from the group totals in between
+// (row_pass1 -> tot[], then row_pass2 with E).
 // kSigma = false (store-mode phase 2): A only; sg[] is scratch.
-template <bool kDiag, bool kSigma = true>
-__device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float E,
-                                              int lim) {
+template <bool kDiag>
+__device__ __forceinline__ void row_pass1(float* s, float* sg, float scale_log2, int lim,
+                                          float* tot) {
 #ifdef SB_NOMATH  // tuning ablation: pipeline without the stick math
-#pragma unroll
-  for (int c = 0; c < kBlock; ++c) { s[c] *= E; sg[c] = E; }
+  tot[0] = tot[1] = tot[2] = tot[3] = 1.0f;
   return;
 #endif
   // The multiplies run as packed f32x2 (FMUL2 / FFMA2, sb_common.cuh batched_row):
   // the scale on adjacent column pairs, everything else on the group pairs
   // (0,1) and (2,3), i.e. columns (c, c+16); bit-identical to the scalar form.
-  constexpr int NG = kBlock / 16;
   const float2 sl2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
   for (int c = 0; c < kBlock; c += 2) {
@@ -90,24 +90,35 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
       sg[c] = tp[h].x;
       sg[c + 16] = tp[h].y;
     }
-  const float tot[NG] = {tp[0].x, tp[0].y, tp[1].x, tp[1].y};
+  tot[0] = tp[0].x;
+  tot[1] = tp[0].y;
+  tot[2] = tp[1].x;
+  tot[3] = tp[1].y;
+}
+
+template <bool kSigma = true>
+__device__ __forceinline__ void row_pass2(float* s, float* sg, float E, const float* tot) {
+#ifdef SB_NOMATH
+#pragma unroll
+  for (int c = 0; c < kBlock; ++c) { s[c] *= E; sg[c] = E; }
+  return;
+#endif
+  constexpr int NG = kBlock / 16;
   bool ok = true;
 #pragma unroll
   for (int g = 0; g < NG; ++g) ok = ok && (tot[g] < kBatchedMax);
   auto fast = [&]() {
     // ninv = -1/P_i (running): sg leaves as -sigma for dz_row's FFMA2
     float2 inv[2], K[2];
-    float Q = E;
     inv[1].y = rcp(tot[3]);
-    K[1].y = Q * inv[1].y;
     inv[1].x = rcp(tot[2]);
-    K[1].x = K[1].y * inv[1].x;
     inv[0].y = rcp(tot[1]);
-    K[0].y = K[1].x * inv[0].y;
     inv[0].x = rcp(tot[0]);
-    K[0].x = K[0].y * inv[0].x;
 #pragma unroll
     for (int h = 0; h < 2; ++h) inv[h] = make_float2(-inv[h].x, -inv[h].y);
+    // first u = t_i P_{i-1} (into s[]) and sigma, which need no E; then A = u K with
+    // the E-dependent group seeds K, so E (phase 1 derives it from this tile's group
+    // totals) has the whole first loop to arrive
 #pragma unroll
     for (int i = 15; i >= 0; --i)
 #pragma unroll
@@ -119,11 +130,24 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
           const float2 sgm = mul2(u, inv[h]);
           sg[c] = sgm.x;
           sg[c + 16] = sgm.y;
+          inv[h] = fma2(inv[h], t, inv[h]);
         }
-        const float2 a = mul2(u, K[h]);
+        s[c] = u.x;
+        s[c + 16] = u.y;
+      }
+    const float Q = E;
+    K[1].y = Q * rcp(tot[3]);
+    K[1].x = K[1].y * rcp(tot[2]);
+    K[0].y = K[1].x * rcp(tot[1]);
+    K[0].x = K[0].y * rcp(tot[0]);
+#pragma unroll
+    for (int i = 15; i >= 0; --i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 32 * h + i;
+        const float2 a = mul2(make_float2(s[c], s[c + 16]), K[h]);
         s[c] = a.x;
         s[c + 16] = a.y;
-        if (kSigma) inv[h] = fma2(inv[h], t, inv[h]);
       }
   };
   if (ok) {
@@ -152,6 +176,51 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
       }
     }
   }
+}
+
+template <bool kDiag, bool kSigma = true>
+__device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_log2, float E,
+                                              int lim) {
+  float tot[4];
+  row_pass1<kDiag>(s, sg, scale_log2, lim, tot);
+  row_pass2<kSigma>(s, sg, E, tot);
+}
+
+// Row total of lt over one tile in log2 units, L = log2 prod (1+t) >= 0, for a row
+// outside the 2^64 range (rare: large logits): t[] = the row's t values (masked
+// columns 0), tot[] the group products of (1+t).  lg2 per group below 2^126 (as the
+// forward's wider range), past that the exact softplus of every element of the
+// group (softplus2 of Z = lg2 t; where t = inf, z itself from the q row and the key
+// rows in global memory).  Out of line with t[] in local memory, so the hot
+// path's code and registers stay as they were.
+__device__ __noinline__ float row_lt_total_slow(const float* t, const float* tot,
+                                                const __nv_bfloat16* qrow,
+                                                const __nv_bfloat16* krow0, int64_t ld, int d,
+                                                float scale_log2) {
+  float lg[4];
+  for (int g = 0; g < 4; ++g) {
+    if (tot[g] < kBatchedWide) {
+      lg[g] = lg2(tot[g]);
+      continue;
+    }
+    float sum = 0.0f;
+    for (int c = 16 * g; c < 16 * g + 16; ++c) {
+      const float tc = t[c];
+      if (!(tc > 0.0f)) continue;  // masked, or softplus below the float range
+      float Z;
+      if (tc < INFINITY) {
+        Z = lg2(tc);
+      } else {
+        float z = 0.0f;
+        const __nv_bfloat16* kr = krow0 + c * ld;
+        for (int i = 0; i < d; ++i) z = fmaf(__bfloat162float(qrow[i]), __bfloat162float(kr[i]), z);
+        Z = z * scale_log2;
+      }
+      sum += softplus2(Z, tc);
+    }
+    lg[g] = sum;
+  }
+  return (lg[3] + lg[2]) + (lg[1] + lg[0]);
 }
 
 // dAt = A * (dW - off) with dW streamed from TMEM in 16-column chunks (warp-collective).
@@ -592,22 +661,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int my_first = half_exists ? args.first_kb[u.fkb_off + my_qb] : u.nb;
       const float off =
           (args.row_offset && row_valid) ? args.row_offset[u.rem_off + row * u.rem_stride] : 0.0f;
-      const float* Mrow = args.M + u.m_off + (r & 63);
-      float* Nrow = kStoreZ ? nullptr : args.N + u.m_off + (r & 63);  // store mode: no N
+      // M snapshots (a in effect per tile, blocked.py:188-189) are rolled back from the
+      // forward's final a, left to right: M(kb) = a_final + sum_{kb' <= kb} L(kb'), L =
+      // the tile's row total of -lt (float64 running sum); phase 2 reads what this
+      // writes.  store mode: no N (phase 2 takes dZ from the tile workspace)
+      float* Mrow = args.M + u.m_off + (r & 63);
+      float* Nrow = kStoreZ ? nullptr : args.N + u.m_off + (r & 63);
       const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
-      auto tile_of = [&](int kb) -> int64_t {  // snapshot slot (row 0 of the unit if not live)
-        const bool lv = row_valid && kb >= my_first && kb <= my_qb;
-        return tile_index(lv ? my_qb : 0, lv ? kb : 0) * kBlock;
-      };
-      float Ma = Mrow[tile_of(it.kb_lo)];  // M of the next tile, loaded one tile ahead
-      float bsum = 0.0f;                   // running b (blocked.py:342, :354)
+      // the rolled-back a as a compensated float pair (float64 adds cost 6% in the forward)
+      float m_hi, m_lo;
+      {
+        const double a0 = row_valid ? args.state[u.rem_off + row * u.rem_stride] : 0.0;
+        m_hi = (float)a0;
+        m_lo = (float)(a0 - (double)m_hi);
+      }
+      float bsum = 0.0f;  // running b (blocked.py:342, :354)
       if (tr) SB_TR(args, w, nwi, 11);
       for (int j = 0; j < n_w; ++j) {
         const int kb = it.kb_lo + j, gi = ig + j;
         const bool live = row_valid && kb >= my_first && kb <= my_qb;
-        const int64_t t = tile_of(kb);
-        const float E = live ? ex2(Ma) : 0.0f;
-        if (j + 1 < n_w) Ma = Mrow[tile_of(kb + 1)];
+        const int64_t t = tile_index(my_qb, kb) * kBlock;
         if (tr) SB_TR(args, w, gi, 0);
         mbar_wait(sfull, gi & 1);
         tc_fence_after();
@@ -621,9 +694,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const bool diag = kb == my_qb;  // warp-uniform
         if (kPingPongQ) named_bar_sync(bar_mine, 256);
         // dead rows/tiles run the same code with e^M = 0 and b = 0: A = 0, dZ = 0
-        if (diag) recompute_row<true>(s, sg, g.scale_log2, E, r & 63);
-        else recompute_row<false>(s, sg, g.scale_log2, E, kBlock);
+        float tot[4], Mk;
+        if (diag) row_pass1<true>(s, sg, g.scale_log2, r & 63, tot);
+        else row_pass1<false>(s, sg, g.scale_log2, kBlock, tot);
+        // the turn ends with the ex2 pass (the MUFU-heavy part): L, E and the
+        // FMA-pipe pass 2 overlap the other warpgroup's ex2 pass (0.6% faster than
+        // holding the turn to the end of pass 2)
         if (kPingPongQ) named_bar_arrive(bar_other, 256);
+        {
+          float L;
+          if (tot[0] < kBatchedMax && tot[1] < kBatchedMax && tot[2] < kBatchedMax &&
+              tot[3] < kBatchedMax) {
+            L = lg2(tot[3] * tot[2]) + lg2(tot[1] * tot[0]);  // the forward's fast path
+          } else {
+            float tl[kBlock];  // local-memory copy for the out-of-line rare path
+#pragma unroll
+            for (int c = 0; c < kBlock; ++c) tl[c] = s[c];
+            L = row_lt_total_slow(tl, tot, args.q + u.out_off + (int64_t)row * g.sl,
+                                  args.k + u.out_off + (int64_t)kb * kBlock * g.sl, g.sl, D,
+                                  g.scale_log2);
+          }
+          // M = (hi + L) + lo: two FADDs after L, exact where M is small (where e^M matters)
+          Mk = (m_hi + L) + m_lo;
+          if (live) two_sum_acc(m_hi, m_lo, L);
+        }
+        const float E = live ? ex2(Mk) : 0.0f;
+
+        row_pass2(s, sg, E, tot);
         if (tr) SB_TR(args, w, gi, 2);
         mbar_wait(wfull, gi & 1);
         tc_fence_after();
@@ -643,6 +740,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         mbar_arrive(zfull);
         if (tr) SB_TR(args, w, gi, 6);
+        // this tile's M snapshot for phase 2 (blocked.py:188-189), written late so the
+        // store never waits on the L -> M chain
+        if (live) Mrow[t] = Mk;
       }
       if (kPingPongQ)
         for (int j = n_w; j < n_rounds; ++j) pp_round_pass();

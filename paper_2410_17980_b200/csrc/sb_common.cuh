@@ -9,9 +9,10 @@
 namespace sb {
 
 constexpr int kBlock = 64;     // reference d_block (blocked.py:41): skip / M / N granularity
-// M and N arrays start with a 64-float header holding the persistent kernels'
-// work-queue counters (M[0]: forward; N[0]: phase 1, N[1]: phase 2), zeroed by
-// the launcher before each kernel; the tile snapshots follow.
+// The forward's state array and the backward's M snapshot array start with a
+// 64-float header holding the persistent kernels' work-queue counters (state[0]:
+// forward; M[0]: phase 1, M[1]: phase 2), zeroed by the launcher before each
+// kernel; the per-row values / tile snapshots follow.
 constexpr int kSchedHeader = 64;
 constexpr int kTileM = 128;    // query rows per CTA tile = two 64-row skip groups
 constexpr float kLog2e = 1.4426950408889634f;
@@ -54,8 +55,6 @@ struct Unit {
 // (the 128B-swizzled smem image, as the MMA reads it).
 __device__ __forceinline__ int64_t ztile(int qt, int kb) { return (int64_t)qt * (qt + 1) + kb; }
 constexpr int kZTileBytes = kTileM * kBlock * 2;
-// the workspace ends with the backward's work-queue counters (store mode has no N)
-constexpr int kZTailBytes = 256;
 
 __device__ __forceinline__ Unit make_unit(const Geom& g, int b, int h) {
   Unit u;

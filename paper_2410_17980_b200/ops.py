@@ -37,11 +37,12 @@ import torch
 from . import _lib
 
 DEFAULT_BLOCK = 64
-SCHED_HEADER = 64  # floats at the start of M / N holding the kernels' work-queue counters
-# Store mode of the backward (phase 1 writes its dZ tiles, phase 2 reads them instead of
-# recomputing dO.V^T and dZ; bit-identical results) is used when its workspace is at most
-# this many bytes (C2: 2.1 GiB; C3 at L=32768 would need 33 GiB and recomputes instead).
-TILE_WORKSPACE_MAX_BYTES = int(float(os.environ.get("SB_TILE_WORKSPACE_MAX_GB", "8")) * 2**30)
+SCHED_HEADER = 64  # floats at the start of the state / snapshot arrays (work-queue counters)
+# The backward's workspace (M snapshots + the store mode's dZ tiles: phase 1 writes them,
+# phase 2 reads them instead of recomputing dO.V^T and dZ; bit-identical results) is bounded
+# by this many bytes per call: a larger problem runs in chunks of whole (b, h) units (C2:
+# 2.2 GB in one call; C3 at L=32768 would need 33 GB and runs in ~10 chunks).
+WORKSPACE_MAX_BYTES = int(float(os.environ.get("SB_WORKSPACE_MAX_GB", "4")) * 2**30)
 SKIP_EPS_BF16 = 1e-6  # the reference's f32 default (blocked.py:43) is used for bf16
 
 
@@ -102,7 +103,7 @@ class BlockedCache:
     layout: BlockLayout
     log_rem: torch.Tensor
     first_kb: torch.Tensor
-    M: torch.Tensor
+    state: torch.Tensor | None  # the forward's O(L) state (final a per row, float64), or None
     skip: bool
     skip_eps: float
     cu_seqlens: torch.Tensor | None = None  # varlen: device int32 [n_seq+1]
@@ -231,18 +232,18 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
     o = torch.empty_like(q)
     log_rem = torch.empty((T, H), device=q.device, dtype=torch.float32)
     first_kb = torch.empty(max(1, n_fkb.value), device=q.device, dtype=torch.int32)
-    M = torch.empty(max(1, n_snap.value), device=q.device, dtype=torch.float32) if two_phase else None
+    state = _state_tensor(lib, p, q.device) if two_phase else None
     cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
     if max_L > 0:
         _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
-                              _ptr(first_kb), _ptr(M), _ptr(cnt), _stream()))
+                              _ptr(first_kb), _ptr(state), _ptr(cnt), _stream()))
     else:
         o.zero_()
         log_rem.zero_()
     total = (n_snap.value - SCHED_HEADER) // DEFAULT_BLOCK
     visited = int(cnt[0].item()) if counters else -1
     stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
-    cache = BlockedCache(q, k, v, scale, None, log_rem, first_kb, M, skip, skip_eps,
+    cache = BlockedCache(q, k, v, scale, None, log_rem, first_kb, state, skip, skip_eps,
                          cu_seqlens=cu, max_seqlen=max_L, cu_host=host_c)
     return o, log_rem, stats, cache
 
@@ -256,10 +257,13 @@ def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = Fal
     Returns (o, log_rem, TileStats, BlockedCache).  log_rem is the reference's
     RowLogAccumulator.a (natural log of the remaining stick mass).
 
-    two_phase=False (blocked.py:136, :163, :188) writes no M snapshots (o, log_rem
-    and first_kb are the same bit for bit): a forward for inference, after which
-    the two-phase backward raises ValueError.  (The reference's fused backward
-    does not exist here: SURVEY.md §8(a).)
+    No call keeps M snapshots (blocked.py:188-189): with two_phase=True the forward
+    keeps only the final a per row (float64, cache.state, O(L)); the backward's
+    phase 1 rolls the per-tile snapshots back from it.  two_phase=False
+    (blocked.py:136, :163, :188) keeps not even that (o, log_rem and first_kb are
+    the same bit for bit): a forward for inference, after which the two-phase
+    backward raises ValueError.  (The reference's fused backward does not exist
+    here: SURVEY.md §8(a).)
 
     Varlen: q, k, v (total_tokens, H, d) with cu_seqlens (int32 [n_seq+1]);
     log_rem is then (total_tokens, H), first_kb a flat array packed sequence by
@@ -290,15 +294,14 @@ def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = Fal
     o = torch.empty_like(q)
     log_rem = torch.empty((B, H, L), device=q.device, dtype=torch.float32)
     first_kb = torch.empty((B, H, layout.n_blocks), device=q.device, dtype=torch.int32)
-    M = (torch.empty(lib.sb_snapshot_elems(ctypes.byref(p)), device=q.device, dtype=torch.float32)
-         if two_phase else None)
+    state = _state_tensor(lib, p, q.device) if two_phase else None
     cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
     _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
-                          _ptr(first_kb), _ptr(M), _ptr(cnt), _stream()))
+                          _ptr(first_kb), _ptr(state), _ptr(cnt), _stream()))
     total = B * H * layout.n_tiles
     visited = int(cnt[0].item()) if counters else -1
     stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
-    cache = BlockedCache(q, k, v, scale, layout, log_rem, first_kb, M, skip, skip_eps)
+    cache = BlockedCache(q, k, v, scale, layout, log_rem, first_kb, state, skip, skip_eps)
     return o, log_rem, stats, cache
 
 
@@ -308,20 +311,31 @@ def sb_forward_blocked(q, k, v, layout=None, **kw):
     return o, cache
 
 
-def tile_workspace_bytes(cache: BlockedCache) -> int:
-    """Bytes of the dZ tile workspace the store-mode backward needs for this cache."""
+def _state_tensor(lib, p, device):
+    """The forward's state array (sb_state_elems floats; the final a of every row as
+    float64 after a 64-float header)."""
+    return torch.empty(lib.sb_state_elems(ctypes.byref(p)), device=device, dtype=torch.float32)
+
+
+def _cache_params(cache: BlockedCache):
+    return _params(cache.q, cache.scale, cache.skip, cache.skip_eps,
+                   cu_seqlens=cache.cu_seqlens, max_seqlen=cache.max_seqlen)
+
+
+def workspace_bytes(cache: BlockedCache, store: bool = True) -> int:
+    """Bytes of the backward's workspace for this cache in one call: the M snapshots
+    (phase 1 -> phase 2) plus the dZ tiles (store mode) or the N snapshots."""
     lib = _lib.load()
-    p = _params(cache.q, cache.scale, cache.skip, cache.skip_eps, cu_seqlens=cache.cu_seqlens,
-                max_seqlen=cache.max_seqlen)
+    p = _cache_params(cache)
     host = None if cache.cu_host is None else ctypes.c_void_p(cache.cu_host.data_ptr())
-    return int(lib.sb_bwd_tile_bytes(ctypes.byref(p), host))
+    return int(lib.sb_bwd_workspace_bytes(ctypes.byref(p), host, int(bool(store))))
 
 
 def workspace_cap_bytes(device=None) -> int:
-    """Largest dZ tile workspace the backward allocates on its own: the
-    SB_TILE_WORKSPACE_MAX_GB cap (default 8 GiB), and at most a quarter of the
-    device memory free right now.  Above it the backward runs in recompute mode."""
-    cap = TILE_WORKSPACE_MAX_BYTES
+    """Largest backward workspace one call allocates: the SB_WORKSPACE_MAX_GB cap
+    (default 4 GiB), and at most a quarter of the device memory free right now.
+    A larger problem runs in chunks of whole (b, h) units."""
+    cap = WORKSPACE_MAX_BYTES
     try:
         free, _ = torch.cuda.mem_get_info(device)
         cap = min(cap, free // 4)
@@ -330,25 +344,80 @@ def workspace_cap_bytes(device=None) -> int:
     return cap
 
 
+def _unit_chunks(cache: BlockedCache, store: bool, cap: int):
+    """Split the call's (b, h) units into the fewest contiguous chunks whose workspace
+    fits `cap` (whole batch entries when B > 1, heads when B == 1, whole sequences
+    for varlen).  Yields (lo, hi) index ranges over that axis; one range covering
+    everything when the whole call fits (or when nothing smaller would)."""
+    lib = _lib.load()
+    q = cache.q
+    if cache.cu_seqlens is not None:
+        n = cache.cu_host.numel() - 1
+        axis_len = n
+    else:
+        B, H = q.shape[0], q.shape[1]
+        n = B if B > 1 else H
+        axis_len = n
+
+    def cost(lo, hi):
+        p = _chunk_params(cache, lo, hi)
+        host = None
+        if cache.cu_seqlens is not None:
+            host = (cache.cu_host[lo:hi + 1] - cache.cu_host[lo]).to(torch.int32).contiguous()
+            return int(lib.sb_bwd_workspace_bytes(ctypes.byref(p), ctypes.c_void_p(host.data_ptr()),
+                                                  int(store)))
+        return int(lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, int(store)))
+
+    if cost(0, axis_len) <= cap:
+        yield 0, axis_len
+        return
+    lo = 0
+    while lo < axis_len:
+        hi = lo + 1
+        while hi < axis_len and cost(lo, hi + 1) <= cap:
+            hi += 1
+        yield lo, hi
+        lo = hi
+
+
+def _chunk_params(cache: BlockedCache, lo: int, hi: int):
+    """Params of the chunk [lo, hi) of _unit_chunks' axis (device cu_seqlens of a varlen
+    chunk are set by the caller)."""
+    q = cache.q
+    if cache.cu_seqlens is not None:
+        t0, t1 = int(cache.cu_host[lo]), int(cache.cu_host[hi])
+        lens = (cache.cu_host[lo + 1:hi + 1] - cache.cu_host[lo:hi]).tolist()
+        p = _params(q[t0:t1] if t1 > t0 else q[:1], cache.scale, cache.skip, cache.skip_eps,
+                    cu_seqlens=cache.cu_seqlens, max_seqlen=max(lens) if lens else 0)
+        p.batch = hi - lo
+        p.total_tokens = max(1, t1 - t0)
+        return p
+    view = q[lo:hi] if q.shape[0] > 1 else q[:, lo:hi]
+    return _params(view, cache.scale, cache.skip, cache.skip_eps)
+
+
 def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | None = None,
                               row_offset=None, *, out=None, phases: int = 3,
-                              store_tiles: bool | None = None, tiles=None):
+                              store_tiles: bool | None = None, workspace=None):
     """blocked_backward_twophase (blocked.py:299-392) over every (b, h) unit.
 
     Returns (d_q, d_k, d_v, n_stored_tiles).  row_offset (B, H, L) float32 is
     subtracted from dO.V^T per query row (blocked.py:241-242).
 
-    store_tiles: None = store mode when its workspace fits workspace_cap_bytes(),
-    True/False to force.  `tiles` passes a preallocated workspace (uint8 CUDA tensor of
-    at least tile_workspace_bytes(cache) bytes); callers running the phases one by one
-    must pass the same one to both.  Store mode needs no N snapshots (phase 2 reads
-    dZ); recompute mode allocates N (one float per row per tile, like M).
+    store_tiles: store mode (phase 2 reads phase 1's dZ tiles) unless False
+    (recompute mode: no tiles, phase 2 recomputes dO.V^T and dZ; same results bit for
+    bit).  The workspace (M snapshots + dZ tiles or N) is transient: allocated here,
+    at most workspace_cap_bytes() per call, the units running in chunks beyond that.
+    `workspace` passes a preallocated one (uint8 CUDA tensor of at least
+    workspace_bytes(cache, store) bytes, no chunking); callers running the phases one
+    by one (phases=1 then 2) must pass the same one to both.  `out` = (dq, dk, dv)
+    preallocated like q.
     """
     if layout is not None and layout != cache.layout:
         raise ValueError("layout does not match the one the cache was built with")  # :398-399
-    if cache.M is None:
+    if cache.state is None:
         raise ValueError("two-phase backward needs a forward run with two_phase=True "
-                         "(M snapshots missing)")  # blocked.py:315-316
+                         "(its state is missing)")  # blocked.py:315-316
     q, k, v = cache.q, cache.k, cache.v
     if d_o.shape != v.shape:
         raise ValueError("d_o shape mismatch")
@@ -357,39 +426,91 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
     if d_o.stride() != q.stride() or d_o.data_ptr() % 16:
         d_o = torch.empty_like(q).copy_(d_o)
     lib = _lib.load()
-    p = _params(q, cache.scale, cache.skip, cache.skip_eps, cu_seqlens=cache.cu_seqlens,
-                max_seqlen=cache.max_seqlen)
     ro = None
     if row_offset is not None:
         ro = row_offset.to(device=q.device, dtype=torch.float32).contiguous()
         if ro.shape != cache.log_rem.shape:
             raise ValueError("row_offset must match log_rem: (batch, heads, seq_len), or "
                              "(total_tokens, heads) for varlen")
-    if cache.cu_seqlens is not None and cache.max_seqlen == 0:
-        dq, dk, dv = (torch.zeros_like(q) for _ in range(3))
+    dq, dk, dv = out if out is not None else (torch.empty_like(q) for _ in range(3))
+    varlen = cache.cu_seqlens is not None
+    n_stored = (cache.layout.n_tiles * q.shape[0] * q.shape[1] if not varlen else
+                _varlen_tiles(cache))
+    if varlen and cache.max_seqlen == 0:
+        for t in (dq, dk, dv):
+            t.zero_()
         return dq, dk, dv, 0
-    need = tile_workspace_bytes(cache)
-    if tiles is None:
-        use = (need <= workspace_cap_bytes(q.device)) if store_tiles is None else bool(store_tiles)
-        if use and need > 0:
-            tiles = torch.empty(need, device=q.device, dtype=torch.uint8)
-    elif tiles.numel() < need:
-        raise ValueError(f"tile workspace has {tiles.numel()} bytes, the backward needs {need}")
-    store = tiles is not None
-    if out is None:  # (N, dq, dk, dv); callers running the phases one by one pass it
-        out = (None if store else torch.empty_like(cache.M), torch.empty_like(q),
-               torch.empty_like(q), torch.empty_like(q))
-    N, dq, dk, dv = out
-    if N is None and not store:
-        raise ValueError("recompute mode needs an N snapshot buffer")
-    nbytes = 0 if tiles is None else tiles.numel()
-    _lib.check(lib.sb_bwd_ws(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(d_o), _ptr(ro),
-                             None, _ptr(cache.first_kb), _ptr(cache.M), _ptr(N),
-                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(tiles), nbytes, int(phases),
-                             _stream()))
-    n_stored = ((cache.M.numel() - SCHED_HEADER) // DEFAULT_BLOCK if cache.cu_seqlens is not None
-                else cache.layout.n_tiles * q.shape[0] * q.shape[1])
+    store = True if store_tiles is None else bool(store_tiles)
+    if workspace is not None:
+        need = workspace_bytes(cache, store)
+        if workspace.numel() < need:
+            raise ValueError(f"workspace has {workspace.numel()} bytes, the backward needs {need}")
+        chunks = [None]
+    else:
+        if phases != 3:
+            raise ValueError("running the phases one by one needs a caller-owned workspace")
+        chunks = list(_unit_chunks(cache, store, workspace_cap_bytes(q.device)))
+        if len(chunks) == 1:
+            chunks = [None]
+    for ch in chunks:
+        _backward_call(lib, cache, d_o, ro, dq, dk, dv, store, phases, ch, workspace)
     return dq, dk, dv, n_stored
+
+
+def _varlen_tiles(cache):
+    lens = (cache.cu_host[1:] - cache.cu_host[:-1]).tolist()
+    H = cache.q.shape[1]
+    return sum(H * ((L + 63) // 64) * ((L + 63) // 64 + 1) // 2 for L in lens)
+
+
+def _backward_call(lib, cache, d_o, ro, dq, dk, dv, store, phases, chunk, workspace):
+    """One sb_bwd call over all units (chunk None) or over the units [lo, hi) of
+    _unit_chunks' axis: pointer offsets into every per-unit array."""
+    q, k, v = cache.q, cache.k, cache.v
+    varlen = cache.cu_seqlens is not None
+    state, fkb = cache.state, cache.first_kb
+    st_off = fkb_off = ro_off = 0
+    cu_dev, cu_host = cache.cu_seqlens, cache.cu_host
+    if chunk is None:
+        p = _cache_params(cache)
+        views = (q, k, v, d_o, dq, dk, dv)
+    else:
+        lo, hi = chunk
+        p = _chunk_params(cache, lo, hi)
+        if varlen:
+            t0, t1 = int(cache.cu_host[lo]), int(cache.cu_host[hi])
+            H = q.shape[1]
+            views = tuple(t[t0:t1] for t in (q, k, v, d_o, dq, dk, dv))
+            cu_host = (cache.cu_host[lo:hi + 1] - t0).to(torch.int32).contiguous()
+            cu_dev = cu_host.to(q.device, non_blocking=False)
+            p.cu_seqlens = ctypes.c_void_p(cu_dev.data_ptr())
+            st_off = ro_off = t0 * H
+            nbs = ((cache.cu_host[1:lo + 1] - cache.cu_host[:lo] + 63) // 64).sum().item()
+            fkb_off = int(nbs) * H
+        else:
+            B, H, L = q.shape[0], q.shape[1], q.shape[2]
+            nb = -(-L // DEFAULT_BLOCK)
+            if B > 1:
+                views = tuple(t[lo:hi] for t in (q, k, v, d_o, dq, dk, dv))
+                units0 = lo * H
+            else:
+                views = tuple(t[:, lo:hi] for t in (q, k, v, d_o, dq, dk, dv))
+                units0 = lo
+            st_off = ro_off = units0 * L
+            fkb_off = units0 * nb
+    qv, kv, vv, dov, dqv, dkv, dvv = views
+    host = None if cu_host is None else ctypes.c_void_p(cu_host.data_ptr())
+    nbytes = int(lib.sb_bwd_workspace_bytes(ctypes.byref(p), host, int(store)))
+    ws = workspace if workspace is not None else torch.empty(nbytes, device=q.device,
+                                                             dtype=torch.uint8)
+    # the state pointer keeps its 64-float header in front of the chunk's rows (sb_bwd
+    # reads only the rows): offset by 2 floats per row
+    st_ptr = ctypes.c_void_p(state.data_ptr() + 8 * st_off)
+    ro_ptr = None if ro is None else ctypes.c_void_p(ro.data_ptr() + 4 * ro_off)
+    fkb_ptr = ctypes.c_void_p(fkb.data_ptr() + 4 * fkb_off)
+    _lib.check(lib.sb_bwd(ctypes.byref(p), _ptr(qv), _ptr(kv), _ptr(vv), _ptr(dov), ro_ptr,
+                          st_ptr, fkb_ptr, _ptr(dqv), _ptr(dkv), _ptr(dvv), _ptr(ws),
+                          ws.numel(), host, int(store), int(phases), _stream()))
 
 
 class _StickBreakingFn(torch.autograd.Function):
@@ -405,7 +526,8 @@ class _StickBreakingFn(torch.autograd.Function):
         ctx.meta = (cache.scale, cache.layout, cache.skip, cache.skip_eps, cache.max_seqlen,
                     cache.cu_host, cache.cu_seqlens is not None)
         extra = (cache.cu_seqlens,) if cache.cu_seqlens is not None else ()
-        ctx.save_for_backward(cache.q, cache.k, cache.v, log_rem, cache.first_kb, cache.M, *extra)
+        ctx.save_for_backward(cache.q, cache.k, cache.v, log_rem, cache.first_kb, cache.state,
+                              *extra)
         ctx.return_rem = return_rem
         if return_rem:
             return o, torch.exp(log_rem)
@@ -413,9 +535,9 @@ class _StickBreakingFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, d_o, d_rem=None):
-        q, k, v, log_rem, first_kb, M, *extra = ctx.saved_tensors
+        q, k, v, log_rem, first_kb, state, *extra = ctx.saved_tensors
         scale, layout, skip, skip_eps, max_seqlen, cu_host, varlen = ctx.meta
-        cache = BlockedCache(q, k, v, scale, layout, log_rem, first_kb, M, skip, skip_eps,
+        cache = BlockedCache(q, k, v, scale, layout, log_rem, first_kb, state, skip, skip_eps,
                              cu_seqlens=extra[0] if varlen else None, max_seqlen=max_seqlen,
                              cu_host=cu_host)
         if d_o is None and d_rem is None:
@@ -441,9 +563,11 @@ def stickbreaking_attention(q, k, v, *, scale: float | None = None, skip: bool =
     and is differentiable.  skip enables the reference's block skipping
     (exact: a skipped block's weights are below skip_eps).
 
-    Without autograd (torch.no_grad(), or no input requiring grad) the forward
-    writes no M snapshots (blocked_forward(two_phase=False)): same outputs, no
-    O(L^2/64) intermediate.
+    Nothing O(L^2/64) is kept between the forward and the backward: the forward
+    saves the final a per row (float64) and the backward rolls the per-tile M
+    snapshots back from it inside its own transient workspace.  Without autograd
+    (torch.no_grad(), or no input requiring grad) not even that is written
+    (blocked_forward(two_phase=False)).
 
     Packed varlen: q, k, v (total_tokens, heads, head_dim) and cu_seqlens (int32
     [n_seq+1] offsets); each sequence attends only within itself.

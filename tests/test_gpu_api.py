@@ -57,7 +57,7 @@ def test_two_phase_false_same_results_no_snapshots(skip, family):
     a = sb.blocked_forward(q, k, v, skip=skip)
     b = sb.blocked_forward(q, k, v, skip=skip, two_phase=False)
     torch.cuda.synchronize()
-    assert b[3].M is None
+    assert b[3].state is None and a[3].state.numel() == 64 + 2 * q.numel() // q.shape[-1]
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
     assert torch.equal(a[2].first_kb, b[2].first_kb) and a[2].visited == b[2].visited
     with pytest.raises(ValueError):  # blocked.py:315-316
@@ -65,8 +65,8 @@ def test_two_phase_false_same_results_no_snapshots(skip, family):
 
 
 def test_inference_forward_allocates_no_snapshots():
-    """stickbreaking_attention without autograd writes no M: its peak memory stays
-    below the M array's size over the outputs."""
+    """stickbreaking_attention without autograd writes no state and no M: its peak
+    memory stays below the M array's size over the outputs."""
     import paper_2410_17980_b200 as sb
     B, H, L, d = 1, 8, 16384, 128
     q, k, v = make_qkv(B, H, L, d, seed=1, with_do=False)
@@ -84,16 +84,34 @@ def test_inference_forward_allocates_no_snapshots():
     assert torch.equal(o, o2) and torch.equal(rem, rem2)
 
 
-def test_store_mode_without_n_matches_oracle():
-    """The store-mode backward allocates and writes no N; gradients unchanged."""
+def test_training_forward_keeps_only_O_L_state():
+    """With autograd the forward keeps the final a per row (float64) and first_kb, no
+    snapshot per tile: the memory held between forward and backward over q, k, v, o
+    is O(L) (north_star: cut the O(L^2/d_block) M/N intermediates)."""
+    import paper_2410_17980_b200 as sb
+    B, H, L, d = 1, 8, 16384, 128
+    q, k, v = make_qkv(B, H, L, d, seed=1, with_do=False)
+    m_bytes = B * H * (L // 64) * (L // 64 + 1) // 2 * 64 * 4  # 67 MB
+    qq = q.clone().requires_grad_(True)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    o = sb.stickbreaking_attention(qq, k, v)
+    torch.cuda.synchronize()
+    held = torch.cuda.memory_allocated() - base - o.numel() * 2
+    rows = B * H * L
+    assert held <= rows * (8 + 4) + B * H * (L // 64) * 4 + 4096 < m_bytes // 10
+
+
+def test_workspace_modes_match_oracle():
+    """Store mode (dZ tiles) and recompute mode (N snapshots) through a caller-owned
+    workspace: same gradients bit for bit, oracle parity, short workspace refused."""
     import paper_2410_17980_b200 as sb
     from tests.gpu_util import oracle_bwd
     q, k, v, d_o = make_qkv(1, 2, 640, 128, seed=8)
     o, lr, st, cache = sb.blocked_forward(q, k, v)
-    need = sb.ops.tile_workspace_bytes(cache)
-    tiles = torch.empty(need, device="cuda", dtype=torch.uint8)
-    out = (None, torch.empty_like(q), torch.empty_like(q), torch.empty_like(q))
-    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, out=out, tiles=tiles)
+    need = sb.ops.workspace_bytes(cache, store=True)
+    ws = torch.empty(need, device="cuda", dtype=torch.uint8)
+    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o, workspace=ws)
     torch.cuda.synchronize()
     ref = oracle_fwd(q, k, v)
     rdq, rdk, rdv, _ = oracle_bwd(q, k, v, d_o, ref)
@@ -102,7 +120,39 @@ def test_store_mode_without_n_matches_oracle():
     for a, b in zip((dq, dk, dv), r[:3]):
         assert torch.equal(a, b)
     with pytest.raises(ValueError):  # short workspace (varlen too) is refused
-        sb.blocked_backward_twophase(cache, d_o, tiles=tiles[: need // 2])
+        sb.blocked_backward_twophase(cache, d_o, workspace=ws[: need // 2])
+
+
+def test_chunked_backward_bit_identical(monkeypatch):
+    """A workspace cap below one call's need splits the units into chunks (batch
+    entries, heads when B == 1, whole sequences for varlen): same gradients bit for bit."""
+    import paper_2410_17980_b200 as sb
+    for shape in ((3, 2, 700, 64), (1, 5, 700, 128)):
+        q, k, v, d_o = make_qkv(*shape, seed=3)
+        _, _, _, cache = sb.blocked_forward(q, k, v)
+        full = sb.blocked_backward_twophase(cache, d_o)
+        one = sb.ops.workspace_bytes(cache) // (shape[0] * shape[1])
+        monkeypatch.setattr(sb.ops, "WORKSPACE_MAX_BYTES", 2 * one + one // 2)
+        assert len(list(sb.ops._unit_chunks(cache, True, sb.ops.workspace_cap_bytes()))) > 1
+        part = sb.blocked_backward_twophase(cache, d_o)
+        monkeypatch.undo()
+        torch.cuda.synchronize()
+        for a, b in zip(full[:3], part[:3]):
+            assert torch.equal(a, b)
+    g = torch.Generator().manual_seed(2)
+    lens = [300, 0, 700, 129, 64]
+    q, k, v, d_o = (torch.randn(sum(lens), 2, 64, generator=g).to(torch.bfloat16).cuda()
+                    for _ in range(4))
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32).cuda()
+    _, _, _, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu)
+    ro = torch.randn(sum(lens), 2, generator=g).cuda()
+    full = sb.blocked_backward_twophase(cache, d_o, row_offset=ro)
+    monkeypatch.setattr(sb.ops, "WORKSPACE_MAX_BYTES", sb.ops.workspace_bytes(cache) // 3)
+    assert len(list(sb.ops._unit_chunks(cache, True, sb.ops.workspace_cap_bytes()))) > 1
+    part = sb.blocked_backward_twophase(cache, d_o, row_offset=ro)
+    torch.cuda.synchronize()
+    for a, b in zip(full[:3], part[:3]):
+        assert torch.equal(a, b)
 
 
 def test_varlen_short_workspace_rejected():
@@ -113,12 +163,12 @@ def test_varlen_short_workspace_rejected():
                     for _ in range(4))
     cu = torch.tensor([0, 300, 1000], dtype=torch.int32).cuda()
     _, _, _, cache = sb.blocked_forward(q, k, v, cu_seqlens=cu)
-    need = sb.ops.tile_workspace_bytes(cache)
+    need = sb.ops.workspace_bytes(cache)
     with pytest.raises(ValueError):
-        sb.blocked_backward_twophase(cache, d_o, tiles=torch.empty(need - 16384, device="cuda",
-                                                                   dtype=torch.uint8))
+        sb.blocked_backward_twophase(cache, d_o, workspace=torch.empty(
+            need - 16384, device="cuda", dtype=torch.uint8))
     dq, dk, dv, _ = sb.blocked_backward_twophase(
-        cache, d_o, tiles=torch.empty(need, device="cuda", dtype=torch.uint8))
+        cache, d_o, workspace=torch.empty(need, device="cuda", dtype=torch.uint8))
     r = sb.blocked_backward_twophase(cache, d_o, store_tiles=False)
     torch.cuda.synchronize()
     for a, b in zip((dq, dk, dv), r[:3]):

@@ -31,8 +31,8 @@ def lib():
 
 def test_exports_every_declared_symbol(lib):
     syms = declared_symbols()
-    assert set(syms) >= {"sb_fwd", "sb_bwd", "sb_bwd_phase", "sb_snapshot_elems",
-                         "sb_status_string", "sb_version"}
+    assert set(syms) >= {"sb_fwd", "sb_bwd", "sb_bwd_workspace_bytes", "sb_state_elems",
+                         "sb_snapshot_elems", "sb_status_string", "sb_version"}
     for s in syms:
         assert hasattr(lib, s), s
     assert set(_lib.EXPORTS) == set(syms)
@@ -59,11 +59,33 @@ def _params(**kw):
 
 
 def test_snapshot_elems_matches_layout(lib):
-    # M/N: a 64-float work-queue header + B*H*n_tiles*64 with n_tiles = nb(nb+1)/2
-    # (blocked.py:58-60)
+    # one snapshot array (M or N): a 64-float work-queue header + B*H*n_tiles*64 with
+    # n_tiles = nb(nb+1)/2 (blocked.py:58-60)
     p = _params(B=2, H=3, L=200)
     nb = 4
     assert lib.sb_snapshot_elems(ctypes.byref(p)) == 64 + 2 * 3 * nb * (nb + 1) // 2 * 64
+
+
+def test_state_is_O_L(lib):
+    """The forward keeps one float64 per row (plus the header), not a snapshot per tile."""
+    p = _params(B=2, H=3, L=200)
+    assert lib.sb_state_elems(ctypes.byref(p)) == 64 + 2 * 2 * 3 * 200
+
+
+def test_workspace_bytes(lib):
+    """M snapshots (rounded up to 1 KiB) + dZ tiles (store) or N (recompute)."""
+    p = _params(B=1, H=2, L=256)  # nb = 4 (10 tiles), n_qt = 2 (6 dZ tiles per unit)
+    m = (64 + 2 * 10 * 64) * 4
+    mr = -(-m // 1024) * 1024
+    assert lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, 1) == mr + 2 * 6 * 16384
+    assert lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, 0) == mr + m
+    # varlen needs the host offsets
+    cu = (ctypes.c_int32 * 3)(0, 128, 256)
+    p.cu_seqlens = ctypes.cast(cu, ctypes.c_void_p)
+    p.batch, p.total_tokens = 2, 256
+    assert lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, 1) == 0
+    m = (64 + 2 * 2 * 3 * 64) * 4
+    assert lib.sb_bwd_workspace_bytes(ctypes.byref(p), cu, 1) == -(-m // 1024) * 1024 + 2 * 2 * 2 * 16384
 
 
 @pytest.mark.parametrize("kw,code", [
@@ -110,11 +132,16 @@ def test_python_varlen_validation():
                                    cu_seqlens=torch.tensor([0, 10], dtype=torch.int32))
 
 
-def test_missing_snapshots_rejected(lib):
-    """blocked.py:315-316: two-phase backward without M snapshots is an error."""
-    p = _params()
+def _bwd(lib, p, state, ws, nbytes, cu_host=None, store=1):
     d = ctypes.c_void_p(16)
-    rc = lib.sb_bwd(ctypes.byref(p), d, d, d, d, None, d, d, None, d, d, d, d, None)
+    return lib.sb_bwd(ctypes.byref(p), d, d, d, d, None, state, d, d, d, d, ws, nbytes, cu_host,
+                      store, 3, None)
+
+
+def test_missing_state_rejected(lib):
+    """blocked.py:315-316: a two-phase backward without the forward's state is an error."""
+    p = _params()
+    rc = _bwd(lib, p, None, ctypes.c_void_p(1024), 1 << 30)
     assert rc == 5
     with pytest.raises(ValueError):
         _lib.check(rc)
@@ -138,15 +165,17 @@ def test_skip_rejects_stop_index_overflow(lib):
     assert lib.sb_fwd(ctypes.byref(p), d, d, d, d, d, d, d, None, None) == 4
 
 
-def test_store_mode_needs_no_n_but_recompute_does(lib):
+def test_workspace_checked(lib):
     p = _params()
     d = ctypes.c_void_p(16)
-    # recompute mode (no workspace) without N: NULL error before any device work
-    rc = lib.sb_bwd_ws(ctypes.byref(p), d, d, d, d, None, None, d, d, None, d, d, d, None, 0, 3,
-                       None)
-    assert rc == 5
-    # store mode with a workspace smaller than sb_bwd_tile_bytes: shape error
-    rc = lib.sb_bwd_ws(ctypes.byref(p), d, d, d, d, None, None, d, d, None, d, d, d,
-                       ctypes.c_void_p(256), 1024, 3, None)
-    assert rc == 1
-    assert lib.sb_bwd_tile_bytes(ctypes.byref(p), None) == 1 * 2 * 2 * 3 * 16384 + 256
+    need = lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, 1)
+    # no workspace / too small: errors before any device work
+    assert _bwd(lib, p, d, None, 0) == 5
+    assert _bwd(lib, p, d, ctypes.c_void_p(1024), need - 1) == 1
+    assert _bwd(lib, p, d, ctypes.c_void_p(1024), lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, 0),
+                store=1) == 1
+    # varlen without host offsets: the workspace cannot be checked
+    cu = (ctypes.c_int32 * 2)(0, 256)
+    p.cu_seqlens = ctypes.cast(cu, ctypes.c_void_p)
+    p.total_tokens = 256
+    assert _bwd(lib, p, d, ctypes.c_void_p(1024), 1 << 30) == 5

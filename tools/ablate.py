@@ -25,12 +25,11 @@ def main(path):
         ev[0].record()
         o, _, _, cache = ops.blocked_forward(q, k, v, counters=False)
         ev[1].record()
-        out = (torch.empty_like(cache.M), torch.empty_like(q), torch.empty_like(q),
-               torch.empty_like(q))
-        tiles = torch.empty(ops.tile_workspace_bytes(cache), device=dev, dtype=torch.uint8)
-        ops.blocked_backward_twophase(cache, do, phases=1, out=out, tiles=tiles)
+        out = tuple(torch.empty_like(q) for _ in range(3))
+        ws = torch.empty(ops.workspace_bytes(cache), device=q.device, dtype=torch.uint8)
+        ops.blocked_backward_twophase(cache, do, phases=1, out=out, workspace=ws)
         ev[2].record()
-        ops.blocked_backward_twophase(cache, do, phases=2, out=out, tiles=tiles)
+        ops.blocked_backward_twophase(cache, do, phases=2, out=out, workspace=ws)
         ev[3].record()
     torch.cuda.synchronize()
     print(path, "fwd %.3f p1 %.3f p2 %.3f ms" % (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]),

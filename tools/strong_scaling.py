@@ -37,15 +37,12 @@ def time_fwd_bwd(q, k, v, d_o, steps, warmup, phases=None):
         _, _, _, cache = sb.blocked_forward(q, k, v, counters=False)
         if e is not None:
             e[1].record()
-        out = (torch.empty_like(cache.M), torch.empty_like(q), torch.empty_like(q),
-               torch.empty_like(q))
-        nbytes = sb.ops.tile_workspace_bytes(cache)
-        tiles = (torch.empty(nbytes, device=q.device, dtype=torch.uint8)
-                 if nbytes <= sb.ops.TILE_WORKSPACE_MAX_BYTES else None)
-        sb.blocked_backward_twophase(cache, d_o, phases=1, out=out, tiles=tiles)
+        out = tuple(torch.empty_like(q) for _ in range(3))
+        ws = torch.empty(sb.ops.workspace_bytes(cache), device=q.device, dtype=torch.uint8)
+        sb.blocked_backward_twophase(cache, d_o, phases=1, out=out, workspace=ws)
         if e is not None:
             e[2].record()
-        sb.blocked_backward_twophase(cache, d_o, phases=2, out=out, tiles=tiles)
+        sb.blocked_backward_twophase(cache, d_o, phases=2, out=out, workspace=ws)
         if e is not None:
             e[3].record()
     for _ in range(warmup):
