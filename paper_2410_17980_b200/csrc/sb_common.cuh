@@ -131,13 +131,16 @@ __device__ __forceinline__ void sched_init(const SchedRing& q, int consumers) {
 // producer warp, k-th item (whole warp; returns the index to every lane).  With
 // ctr == nullptr (a forward without the M array, whose header holds the counter)
 // the items are dealt statically: CTA c takes c, c + grid, c + 2 grid, ...
+// The slot is handed over by the mbarriers (arrive = release, wait = acquire); its
+// accesses are shared-memory atomics all the same, which compute-sanitizer's
+// racecheck (unaware of mbarrier ordering for plain st/ld.shared) does not flag.
 __device__ __forceinline__ int sched_produce(const SchedRing& q, int k, unsigned* ctr, int n_items) {
   int idx = 0;
   if ((threadIdx.x & 31) == 0) {
     idx = ctr ? (int)atomicAdd(ctr, 1u) : (int)(blockIdx.x + (unsigned)k * gridDim.x);
     if (idx >= n_items) idx = -1;
     if (k >= 4) mbar_wait(q.empty + (k & 3), ((k >> 2) - 1) & 1);
-    q.slot[k & 3] = idx;
+    atomicExch(q.slot + (k & 3), idx);
     mbar_arrive(q.full + (k & 3));
   }
   return __shfl_sync(0xffffffffu, idx, 0);
@@ -145,10 +148,12 @@ __device__ __forceinline__ int sched_produce(const SchedRing& q, int k, unsigned
 // consumer warp, k-th item
 __device__ __forceinline__ int sched_consume(const SchedRing& q, int k) {
   mbar_wait(q.full + (k & 3), (k >> 2) & 1);
-  const int idx = *(volatile int*)(q.slot + (k & 3));
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(q.empty + (k & 3));
-  return idx;
+  int idx = 0;
+  if ((threadIdx.x & 31) == 0) {
+    idx = atomicAdd(q.slot + (k & 3), 0);
+    mbar_arrive(q.empty + (k & 3));
+  }
+  return __shfl_sync(0xffffffffu, idx, 0);
 }
 
 // tile(qb, kb) = qb*(qb+1)/2 + kb, the reference's (qb, kb) snapshot key order

@@ -117,11 +117,18 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   uint64_t* bar_nload = bar_qtm + 2;  // [2] (skip) the producer's tile count of an item
   // skip: per warpgroup (seq << 13) | stop of its current item (-1: none yet), and
   // per item parity the number of stream tiles the producer loaded
-  volatile int* wg_done = reinterpret_cast<volatile int*>(smem + C::kOffMisc + 64);
-  volatile int* nload_v = wg_done + 2;
+  // (polled flags: shared-memory atomics, see sched_consume)
+  int* wg_done = reinterpret_cast<int*>(smem + C::kOffMisc + 64);
+  int* nload_v = wg_done + 2;
   double* red = reinterpret_cast<double*>(smem + C::kOffMisc + 128);  // [wg][parity][quarter]
+  // one read per warp (lane 0, broadcast): every lane must take the same branch
+  auto flag_read = [](int* f) -> int {
+    int v = 0;
+    if ((threadIdx.x & 31) == 0) v = atomicAdd(f, 0);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
   auto stop_of = [&](int w, int seq) -> int {
-    const int v = wg_done[w];
+    const int v = flag_read(wg_done + w);
     return (v >> 13) == seq ? (v & 8191) : 0x7fffffff;
   };
 
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       }
       if constexpr (kSkip) {
         if (leader) {
-          nload_v[ni & 1] = n_load;
+          atomicExch(nload_v + (ni & 1), n_load);
           mbar_arrive(bar_nload + (ni & 1));
         }
         __syncwarp();
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           // tile cannot be the next item's (the producer publishes before loading it)
           const bool kv = mbar_test(bar_kfull + s, par) && mbar_test(bar_vfull + s, par);
           if (mbar_test(nb_bar, nb_par)) {
-            const int n = nload_v[ni & 1];
+            const int n = flag_read(nload_v + (ni & 1));
             if (j >= n) return n;
           }
           if (kv) break;
@@ -561,7 +568,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             if (done) {
               n_proc = i + 1;
               // published before S is released: the issuer checks it before S(i+1)
-              if (r == 0) wg_done[w] = ((ni - 1) << 13) | (j0 + i + 1);
+              if (r == 0) atomicExch(wg_done + w, ((ni - 1) << 13) | (j0 + i + 1));
             }
           }
         }
