@@ -210,7 +210,9 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   a.state = state ? reinterpret_cast<double*>(state + sb::kSchedHeader) : nullptr;
   a.counters = tile_counters;
   const double eps = p->skip_eps != 0.0f ? (double)p->skip_eps : 1e-6;
-  a.log_eps = std::log(eps);
+  const double le2 = std::log(eps) / std::log(2.0);
+  a.log_eps2_hi = (float)le2;
+  a.log_eps2_lo = (float)(le2 - (double)a.log_eps2_hi);
   a.trace = g_trace;
   a.sched = reinterpret_cast<unsigned*>(state);  // NULL: items dealt statically
   int rc = sb::fwd_pp_dispatch(p->head_dim, p->skip != 0, tq, tk, tv, a,

@@ -12,7 +12,8 @@ struct FwdArgs {
   double* state;         // [B,H,L] final a per row (log2 units, float64): the O(L) state
                          // the backward rolls the M snapshots back from; nullable
   unsigned long long* counters;  // [2]: visited tiles, total tiles (nullable)
-  double log_eps;        // log(skip_eps)
+  float log_eps2_hi;     // log2(skip_eps) as a float pair (hi + lo)
+  float log_eps2_lo;
   uint32_t* trace;       // SB_TRACE builds only (libsbattn_trace.so); null otherwise
   unsigned* sched;       // work-queue counter (state header), zeroed before the launch
 };

@@ -185,38 +185,6 @@ __device__ __forceinline__ float softplus2(float Z, float t) {
 // group of columns (exact slow path if that product underflows).
 constexpr float kProdFloor = 7.52316384526264e-37f;  // 2^-120: lg2 of a normal product is exact enough
 
-// sigma = t/(1+t) and r = 1/(1+t); fminf drops the NaN of inf*0 when t overflows (sigma -> 1)
-__device__ __forceinline__ void sigma_r(float t, float& sg, float& r) {
-  r = rcp(1.0f + t);
-  sg = fminf(t * r, 1.0f);
-}
-
-// Right-to-left pass over n columns of one row: zs[c] holds the raw dot
-// products on entry and Z = z*log2(e) on exit; w[c] = sigma_c * prod_{c<c'<n} r_c',
-// sg[c] = sigma_c (if non-null). Columns c >= lim (diagonal tiles only) are masked:
-// sigma = 0, r = 1. Returns prod r over the group.
-template <int n, bool kDiag>
-__device__ __forceinline__ float prod_pass(float* zs, float* w, float* sg, float scale_log2,
-                                           int c0, int lim) {
-  float Ql = 1.0f;
-#pragma unroll
-  for (int c = n - 1; c >= 0; --c) {
-    const float Z = zs[c] * scale_log2;
-    zs[c] = Z;
-    float s, r;
-    sigma_r(ex2(Z), s, r);
-    if (kDiag) {
-      const bool on = c0 + c < lim;
-      s = on ? s : 0.0f;
-      r = on ? r : 1.0f;
-    }
-    if (sg) sg[c] = s;
-    w[c] = s * Ql;
-    Ql *= r;
-  }
-  return Ql;
-}
-
 // Batched-reciprocal product form for one row of a 64-column tile (forward).
 // Within a group of 16 columns, with P_i = prod_{k<=i} (1+t_k):
 //   A_i = sigma_i * Q * prod_{k>i} r_k = t_i * Q * P_{i-1} / P_15,
@@ -256,18 +224,47 @@ __device__ __forceinline__ float2 x2_pass2_step(const float* s, uint32_t* pk, in
   return F;
 }
 
-// The multiplies run as packed f32x2 (FMUL2 / FFMA2: two lanes per FMA-pipe
-// instruction, each rounded exactly like the scalar op, so the results are the
-// scalar form's bit for bit): the scale on adjacent column pairs, the product and
-// seed chains on the group pairs (0,1) and (2,3).  That halves the FMA-pipe work,
-// which otherwise matches the MUFU's (tools/ubench/ub_rowmath.cu).
-template <bool kDiag>
+// The row's log2 prod (1+t) over a tile from batched_row<kDiag, true>'s Em, accurate
+// for the skip decisions (blocked.py:175-176): e = prod (1+t) - 1 per group carries no
+// 1 + t rounding (which for t ~ e^-8 would cost ~1e-4 of each softplus); log1p2_x2
+// per group pair.  The skip-on forward evaluates it after releasing S; with the e
+// chain one FMA-pipe op per element and one lg2 per group, where the exact
+// per-element softplus costs a MUFU lg2 per element.
+__device__ __forceinline__ float2 log1p2_x2(float2 e, float2 P);
+__device__ __forceinline__ float lt_row_from_em(const float2* Em) {
+  const float2 one = make_float2(1.0f, 1.0f);
+  const float2 l0 = log1p2_x2(Em[0], add2(Em[0], one)), l1 = log1p2_x2(Em[1], add2(Em[1], one));
+  return (l0.x + l0.y) + (l1.x + l1.y);
+}
+
+// log2(1 + e) for two groups (e >= 0: a group's prod (1+t) - 1, P = 1 + e): the
+// series below 1/16, where lg2.approx of P would carry an absolute error comparable
+// to the value, else lg2(P).  Branch-free (a warp-uniform branch around the lg2
+// measured slower), the series on both lanes at once.
+__device__ __forceinline__ float2 log1p2_x2(float2 e, float2 P) {
+  const auto f2 = [](float v) { return make_float2(v, v); };
+  float2 p = fma2(e, f2(-1.0f / 6.0f), f2(1.0f / 5.0f));
+  p = fma2(p, e, f2(-1.0f / 4.0f));
+  p = fma2(p, e, f2(1.0f / 3.0f));
+  p = fma2(p, e, f2(-1.0f / 2.0f));
+  p = fma2(p, e, f2(1.0f));
+  const float2 small = mul2(p, mul2(e, f2(kLog2e)));
+  const float b0 = lg2(P.x), b1 = lg2(P.y);
+  return make_float2(e.x < 0.0625f ? small.x : b0, e.y < 0.0625f ? small.y : b1);
+}
+
+// kEm (the skip-on forward): also Em = per group prod (1+t) - 1, carried as
+// e_i = e_{i-1} + t_i P_{i-1} next to the P chain (for lt_row_from_em: no 1 + t
+// rounding; the product only needs relative accuracy).
+template <bool kDiag, bool kEm = false>
 __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_log2, int lim,
-                                            float& Q, float& Dhi, float& Dlo) {
+                                            float& Q, float& Dhi, float& Dlo,
+                                            float2* Em = nullptr) {
 #ifdef SB_NOMATH  // tuning ablation: pipeline without the stick math
 #pragma unroll
   for (int c = 0; c < kBlock; c += 2) pk[c >> 1] = pack_bf16(s[c] * Q, s[c + 1] * Q);
   Dhi = Dlo = 1.0f;
+  if (kEm) Em[0] = Em[1] = make_float2(0.0f, 0.0f);
   return true;
 #endif
   // pass 1: t into s[], then the group products (two f32x2 chains of group pairs)
@@ -284,10 +281,16 @@ __device__ __forceinline__ bool batched_row(float* s, uint32_t* pk, float scale_
     s[c + 1] = t1;
   }
   float2 P[2] = {make_float2(1.0f, 1.0f), make_float2(1.0f, 1.0f)};
+  if (kEm) Em[0] = Em[1] = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int i = 0; i < 16; ++i)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) P[h] = fma2(P[h], make_float2(s[32 * h + i], s[32 * h + 16 + i]), P[h]);
+    for (int h = 0; h < 2; ++h) {
+      const float2 t2 = make_float2(s[32 * h + i], s[32 * h + 16 + i]);
+      // e_i = e_{i-1} + t_i P_{i-1} (= P_i - 1 without forming 1 + t): one FFMA2
+      if (kEm) Em[h] = fma2(t2, P[h], Em[h]);
+      P[h] = fma2(P[h], t2, P[h]);
+    }
   // group seeds F_g = Q_g / P_g, right to left
   float2 F[2];
   F[1].y = Q * rcp(P[1].y);
@@ -349,124 +352,6 @@ __device__ __forceinline__ bool batched_row_wide(float* s, uint32_t* pk, float s
     }
   lsum = (lg2(P[3]) + lg2(P[2])) + (lg2(P[1]) + lg2(P[0]));
   return true;
-}
-
-// softplus2 on two lanes (FFMA2 / FMUL2 / FADD2): per lane exactly softplus2's
-// operations, so the skip decisions built on it stay bit-exact.
-__device__ __forceinline__ float2 softplus2_x2(float2 Z, float2 t) {
-  const auto f2 = [](float v) { return make_float2(v, v); };
-  float2 p = fma2(t, f2(-1.0f / 6.0f), f2(1.0f / 5.0f));
-  p = fma2(p, t, f2(-1.0f / 4.0f));
-  p = fma2(p, t, f2(1.0f / 3.0f));
-  p = fma2(p, t, f2(-1.0f / 2.0f));
-  p = fma2(p, t, f2(1.0f));
-  const float2 small = mul2(p, mul2(t, f2(kLog2e)));
-  const float2 onep = add2(f2(1.0f), t);
-  float2 sp;
-  sp.x = t.x < 0.0625f ? small.x : lg2(onep.x);
-  sp.y = t.y < 0.0625f ? small.y : lg2(onep.y);
-  sp.x = Z.x > kSoftplusThr2 ? Z.x : sp.x;
-  sp.y = Z.y > kSoftplusThr2 ? Z.y : sp.y;
-  return sp;
-}
-
-// Skip-on forward (sb_fwd_pp_kernel<D, true>): the row's exact sum of lt for the
-// skip decisions, with the exact-path kernel's arithmetic (log_pass + the group
-// totals added 0..3: per 16-column group, right to left, f32), and t = 2^Z left
-// in s[] for the product form (0 where masked).  Returns the sum in log2 units.
-// The elementwise part runs on adjacent column pairs as f32x2; the sums keep
-// their order.
-template <bool kDiag>
-__device__ __forceinline__ float exact_lt_row(float* s, float scale_log2, int lim) {
-  const float2 sl2 = make_float2(scale_log2, scale_log2);
-  float tot = 0.0f;
-#pragma unroll
-  for (int g = 0; g < kBlock / 16; ++g) {
-    float cum = 0.0f;
-#pragma unroll
-    for (int c = 14; c >= 0; c -= 2) {
-      const int col = 16 * g + c;
-      const float2 Z = mul2(make_float2(s[col], s[col + 1]), sl2);
-      const float2 t = make_float2(ex2(Z.x), ex2(Z.y));
-      const float2 sp = softplus2_x2(Z, t);
-      const bool m0 = !kDiag || col < lim, m1 = !kDiag || col + 1 < lim;
-      cum -= m1 ? sp.y : 0.0f;
-      cum -= m0 ? sp.x : 0.0f;
-      s[col] = m0 ? t.x : 0.0f;
-      s[col + 1] = m1 ? t.y : 0.0f;
-    }
-    tot += cum;
-  }
-  return tot;
-}
-
-// batched_row's product form from precomputed t (s[] = t, masked columns 0): A
-// into pk with Q = e^a carried right to left.  False if a group product reached
-// 2^64 (the caller redoes the row per element).  Scalar: the f32x2 form spills in
-// the skip-on kernel.
-__device__ __forceinline__ bool batched_from_t(const float* s, uint32_t* pk, float Q,
-                                               float limit = kBatchedMax) {
-  const float q_in = Q;
-  constexpr int NG = kBlock / 16;
-  float P[NG];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) P[g] = 1.0f;
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-#pragma unroll
-    for (int g = 0; g < NG; ++g) P[g] = fmaf(P[g], s[16 * g + i], P[g]);
-  bool ok = true;
-#pragma unroll
-  for (int g = 0; g < NG; ++g) ok = ok && (P[g] < limit);
-  float F[NG];
-#pragma unroll
-  for (int g = NG - 1; g >= 0; --g) {
-    F[g] = Q * rcp(P[g]);
-    Q = F[g];
-  }
-  if (limit > kBatchedMax) ok = ok && batched_seed_ok(Q, q_in);  // the wider range
-#pragma unroll
-  for (int i = 0; i < 16; i += 2)
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int c = 16 * g + i;
-      const float a0 = s[c] * F[g];
-      F[g] = fmaf(F[g], s[c], F[g]);
-      const float a1 = s[c + 1] * F[g];
-      F[g] = fmaf(F[g], s[c + 1], F[g]);
-      pk[c >> 1] = pack_bf16(a0, a1);
-    }
-  return ok;
-}
-
-// Log-space variant (exact skip path, blocked.py:179-186 restated): Z on exit in
-// zs[c], inclusive in-group suffix sums of lt (log2 units) in cl[c]; returns the
-// group total. Branch-free: masked columns contribute 0.
-template <int n, bool kDiag>
-__device__ __forceinline__ float log_pass(float* zs, float* cl, float scale_log2, int c0, int lim) {
-  float cum = 0.0f;
-#pragma unroll
-  for (int c = n - 1; c >= 0; --c) {
-    const float Z = zs[c] * scale_log2;
-    zs[c] = Z;
-    const float sp = softplus2(Z, ex2(Z));
-    cum -= (!kDiag || c0 + c < lim) ? sp : 0.0f;
-    cl[c] = cum;
-  }
-  return cum;
-}
-
-// log2 of a group's product of r; exact sum of -softplus when it underflowed.
-template <int n, bool kDiag>
-__device__ __forceinline__ float group_log2(float P, const float* Z, int c0, int lim) {
-  if (P >= kProdFloor) return lg2(P);
-  float s = 0.0f;
-#pragma unroll
-  for (int c = 0; c < n; ++c) {
-    const float sp = softplus2(Z[c], ex2(Z[c]));
-    s -= (!kDiag || c0 + c < lim) ? sp : 0.0f;
-  }
-  return s;
 }
 
 }  // namespace sb

@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
   // (polled flags: shared-memory atomics, see sched_consume)
   int* wg_done = reinterpret_cast<int*>(smem + C::kOffMisc + 64);
   int* nload_v = wg_done + 2;
-  double* red = reinterpret_cast<double*>(smem + C::kOffMisc + 128);  // [wg][parity][quarter]
+  // skip votes [wg][round parity][quarter]: (round << 1) | vote, polled like the flags
+  int* votes = reinterpret_cast<int*>(smem + C::kOffMisc + 128);
   // one read per warp (lane 0, broadcast): every lane must take the same branch
   auto flag_read = [](int* f) -> int {
     int v = 0;
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     mbar_init(bar_qtm + 1, 128);
     mbar_init(bar_nload, 1);
     mbar_init(bar_nload + 1, 1);
+    for (int i = 0; i < 16; ++i) votes[i] = -2;  // round -1: none yet
     wg_done[0] = wg_done[1] = -1;
     sched_init(sq, 10);  // consumers: stick warps 0-7, issuer warps 9-10
     fence_mbar_init();
@@ -194,25 +196,14 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       int n_load = it.n_s;
       for (int j = 0; j < it.n_s; ++j, ++jg) {
         const int s = jg % ST;
-        if constexpr (kSkip) {
-          // stop once both warpgroups are done; poll while waiting for the slot (its
-          // release may depend on this item's tile count when they are)
-          bool stop = false;
-          const long long t0 = clock64();
-          for (;;) {
-            if (watchdog_expired(t0)) __trap();  // deadlock: fail loudly (sm100.cuh)
-            if (j > 0 && stop_of(0, ni) <= j && (!it.has1 || stop_of(1, ni) <= j)) {
-              stop = true;
-              break;
-            }
-            if (jg < ST || mbar_test(bar_kvempty + s, ((jg / ST) - 1) & 1)) break;
-          }
-          if (stop) {
-            n_load = j;
-            break;
-          }
-        } else {
-          if (jg >= ST) mbar_wait(bar_kvempty + s, ((jg / ST) - 1) & 1);
+        // wait for the slot: it is always freed, also after both warpgroups stopped
+        // (their issuers release every loaded tile they no longer read as it lands)
+        if (jg >= ST) mbar_wait(bar_kvempty + s, ((jg / ST) - 1) & 1);
+        // skip: stop once both warpgroups are done (their stops are published before
+        // they release S; one look per tile, the ring slack absorbs the lag)
+        if (kSkip && j > 0 && stop_of(0, ni) <= j && (!it.has1 || stop_of(1, ni) <= j)) {
+          n_load = j;
+          break;
         }
         const int kb = it.kbhi1 - j;
         if (leader) {
@@ -274,6 +265,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           }
           if (kv) break;
           if (watchdog_expired(t0)) __trap();  // deadlock: fail loudly (sm100.cuh)
+          __nanosleep(64);  // back off (the issuer warps share SMSPs with stick warps)
         }
         if (leader) mbar_arrive(bar_kvempty + s);
         __syncwarp();
@@ -389,7 +381,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
     const float sl2 = g.scale_log2;
     const bool tr = quarter == 0 && lane == 0;
     if (tr) SB_TR(args, w, 0, 14);
-    int ig = 0, nwi = 0, ni = 0;
+    int ig = 0, nwi = 0, ni = 0, nv = 0;  // nv: skip-vote rounds of this warpgroup
     for (int k = 0;; ++k) {
       const int idx = sched_consume(sq, k);
       if (idx < 0) break;
@@ -424,16 +416,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const bool row_valid = row < u.L;
       const int kbhi = w ? it.kbhi1 : it.kbhi0;
       const int n_w = kbhi + 1;
-      // running remaining mass a: a2 float32 log2 (the tile math) with a2_lo its
-      // compensation (skip off: a2 + a2_lo is the backward's state); skip on: a_d
-      // float64 natural log, the exact decision sums, which a2 follows
+      // running remaining mass a (log2 units): a2 float32 (the tile math) with a2_lo
+      // its compensation; a2 + a2_lo is the backward's state and, skip on, what the
+      // skip decisions compare
       float a2 = 0.0f, a2_lo = 0.0f;
-      double a_d = 0.0;
       // skip: the two query blocks' sweep state, and (thread (r & 63) == 0) the
       // block's leftmost visited tile and count
       const int qb0 = 2 * qt, half = r >> 6;
       bool act[2] = {qb0 < u.nb, qb0 + 1 < u.nb};
       int lowest = my_qb, visited = 0, n_proc = n_w;
+      bool my_vote = false;  // skip: this warp's latest vote (all its rows below log eps)
       const int j0 = it.kbhi1 - kbhi;  // stream index of this warpgroup's first tile
       for (int i = 0; i < n_w; ++i) {
         const int kb = kbhi - i, gi = ig + i;
@@ -449,46 +441,64 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         bool slow = false;
         const bool diag = kb == my_qb;
         const int lim = diag ? (r & 63) : kBlock;
-        const float a2_in = a2;
+        bool done = false;
+        if (kSkip && i > 0 && my_vote) {
+          // skip check for this tile (blocked.py:175-176) on a after the previous one:
+          // every valid row of a query block below log eps <=> the block's max is.
+          // The four warps voted at the end of tile i-1 (one __all_sync each, vote
+          // round rv = nv-1), each into its slot of the round's parity as one word
+          // (rv << 1) | vote; a slot cannot move on to round rv+2 before this warp
+          // released S(i).  a only decreases, so votes are monotone: a warp whose
+          // own vote is false knows its block goes on and need not look (nor can the
+          // warpgroup be done); the others wait for the four round-rv words (the
+          // other block's state only matters for `done`, its latest round tells it).
+          // A warpgroup whose blocks both stopped runs this tile as a no-op (S(i) is
+          // already issued) and publishes its stop before releasing S, so S(i+1) is
+          // never issued.
+          const int rv = nv - 1;
+          int vbits = 0;
+          if (lane == 0) {
+            int* slot = votes + (w * 2 + (rv & 1)) * 4;
+            const long long t0 = clock64();
+            for (int q = 0; q < 4; ++q) {
+              int v;
+              while (((v = atomicAdd(slot + q, 0)) >> 1) != rv)
+                if (watchdog_expired(t0)) __trap();  // deadlock: fail loudly (sm100.cuh)
+              vbits |= (v & 1) << q;
+            }
+          }
+          vbits = __shfl_sync(0xffffffffu, vbits, 0);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            if (act[hh] && kb < qb0 + hh && ((vbits >> (2 * hh)) & 3) == 3) act[hh] = false;
+          done = !act[0] && !act[1];
+          if (done) {
+            n_proc = i + 1;
+            if (r == 0) atomicExch(wg_done + w, ((ni - 1) << 13) | (j0 + i + 1));
+          }
+        }
         // warp-uniform: a warp's rows share one 64-row half
-        if ((!kSkip || act[half]) && kb <= my_qb) {
-          if constexpr (kSkip) {
-            // exact lt sum first (t left in s[]), then the product form from t
-            const float tot = diag ? exact_lt_row<true>(s, sl2, lim) : exact_lt_row<false>(s, sl2, lim);
-            slow = !batched_from_t(s, pk, ex2(a2));
-            a_d += (double)tot * (double)kLn2;
-            a2 = (float)(a_d * 1.4426950408889634);
+        const bool math = (!kSkip || act[half]) && kb <= my_qb;
+        float2 Em[2];  // skip on: per group prod (1+t) - 1 (batched_row)
+        if (math) {
+          // batched reciprocal (sb_common.cuh): one rcp per 16 columns (leaves t in s[])
+          float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
+          slow = diag ? !batched_row<true, kSkip>(s, pk, sl2, lim, Q, Dhi, Dlo, Em)
+                      : !batched_row<false, kSkip>(s, pk, sl2, kBlock, Q, Dhi, Dlo, Em);
+          // skip off: the tile's row total of lt (phase 1 recomputes it with the same
+          // operations), accumulated compensated: a2 + a2_lo.  Skip on: the accurate
+          // total for the decisions, after S is released (below)
+          if (!kSkip && !slow) two_sum_acc(a2, a2_lo, -(lg2(Dhi) + lg2(Dlo)));
+          if (kSkip) {
             lowest = kb;
             ++visited;
-          } else {
-            // batched reciprocal (sb_common.cuh): one rcp per 16 columns
-            float Q = ex2(a2), Dhi = 1.0f, Dlo = 1.0f;
-            slow = diag ? !batched_row<true>(s, pk, sl2, lim, Q, Dhi, Dlo)
-                        : !batched_row<false>(s, pk, sl2, kBlock, Q, Dhi, Dlo);
-            // the tile's row total of lt (phase 1 recomputes it with the same operations);
-            // the float32 a2 feeds the next tile, the float64 shadow only the state
-            if (!slow) two_sum_acc(a2, a2_lo, -(lg2(Dhi) + lg2(Dlo)));
           }
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
         }
-        if (kSkip && __any_sync(0xffffffffu, slow)) {
-          // a group product reached 2^64: the wider batched range, else the
-          // per-element product form from t (a is exact either way)
-          if (slow) slow = !batched_from_t(s, pk, ex2(a2_in), kBatchedWide);
-          if (slow) {
-            float Ql = ex2(a2_in), an = 0.0f;
-#pragma unroll
-            for (int c = kBlock - 1; c >= 0; --c) {
-              const float rr = rcp(1.0f + s[c]);
-              const float a = fminf(s[c] * rr, 1.0f) * Ql;  // t = inf: sigma = 1
-              Ql *= rr;
-              if (c & 1) an = a;
-              else pk[c >> 1] = pack_bf16(a, an);
-            }
-          }
-        } else if (!kSkip && __any_sync(0xffffffffu, slow)) {
+        const bool batched_ok = math && !slow;  // a not yet updated for slow rows
+        if (__any_sync(0xffffffffu, slow)) {
           // a group product of (1+t) reached 2^64: per-element path for those rows
           // (S is still in TMEM: s_empty not yet signalled)
           tmem_ld32(tS, s);
@@ -548,30 +558,6 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
             two_sum_acc(a2, a2_lo, lt);
           }
         }
-        bool done = false;
-        if constexpr (kSkip) {
-          // skip check for the next tile (blocked.py:175-176) on a after this one:
-          // max over each 64-row query block, exchanged between its two warps
-          if (i + 1 < n_w) {
-            double m = row_valid ? a_d : -INFINITY;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-            double* rw = red + (w * 2 + (gi & 1)) * 4;
-            if (lane == 0) rw[quarter] = m;
-            named_bar_sync(1 + w, 128);
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const double mh = fmax(rw[2 * hh], rw[2 * hh + 1]);
-              if (act[hh] && kb - 1 < qb0 + hh && mh < args.log_eps) act[hh] = false;
-            }
-            done = !act[0] && !act[1];
-            if (done) {
-              n_proc = i + 1;
-              // published before S is released: the issuer checks it before S(i+1)
-              if (r == 0) atomicExch(wg_done + w, ((ni - 1) << 13) | (j0 + i + 1));
-            }
-          }
-        }
         tc_fence_before();
         mbar_arrive(sempty);  // S(i+1) may overwrite the buffer now
         if (tr) SB_TR(args, w, gi, 2);
@@ -585,6 +571,22 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         fence_proxy_async_smem();
         mbar_arrive(pfull + (gi & 1));
         if (tr) SB_TR(args, w, gi, 4);
+        if (kSkip && !done) {
+          // the row total of lt for the skip decisions (blocked.py:175-176), after the
+          // tile's S and P turnaround (fast rows; the slow ones updated a already)
+          if (batched_ok) two_sum_acc(a2, a2_lo, -lt_row_from_em(Em));
+          // this warp's vote for the next tile's check: all its valid rows' a below log
+          // eps (a - log eps from the compensated pairs: exact near a tie, where a2 and
+          // the threshold's high part are within a factor 2).  Vote round nv of this
+          // warpgroup: slot nv & 1
+          if (i + 1 < n_w) {
+            const bool below =
+                !row_valid || (a2 - args.log_eps2_hi) + (a2_lo - args.log_eps2_lo) < 0.0f;
+            my_vote = __all_sync(0xffffffffu, below);
+            if (lane == 0) atomicExch(votes + (w * 2 + (nv & 1)) * 4 + quarter, (nv << 1) | my_vote);
+            ++nv;
+          }
+        }
         if (done) break;
       }
       // epilogue: O rows leave in 64-column halves through this warp's 4 KB slice
@@ -609,10 +611,10 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       }
       if (row_valid) {
         const int64_t ri = u.rem_off + row * u.rem_stride;
-        if (!kSkip) a_d = (double)a2 + (double)a2_lo;
-        args.log_rem[ri] = kSkip ? (float)a_d : (float)(a_d * (double)kLn2);
+        const double a_d = (double)a2 + (double)a2_lo;
+        args.log_rem[ri] = (float)(a_d * (double)kLn2);
         // the backward's state: final a in log2 units, float64
-        if (args.state) args.state[ri] = kSkip ? a_d * 1.4426950408889634 : a_d;
+        if (args.state) args.state[ri] = a_d;
       }
       if (my_qb < u.nb && (r & 63) == 0) {
         args.first_kb[u.fkb_off + my_qb] = kSkip ? lowest : 0;

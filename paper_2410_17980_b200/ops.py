@@ -452,9 +452,24 @@ def blocked_backward_twophase(cache: BlockedCache, d_o, layout: BlockLayout | No
         chunks = list(_unit_chunks(cache, store, workspace_cap_bytes(q.device)))
         if len(chunks) == 1:
             chunks = [None]
+        # one allocation for every chunk
+        workspace = torch.empty(max(_chunk_bytes(lib, cache, store, c) for c in chunks),
+                                device=q.device, dtype=torch.uint8)
     for ch in chunks:
         _backward_call(lib, cache, d_o, ro, dq, dk, dv, store, phases, ch, workspace)
     return dq, dk, dv, n_stored
+
+
+def _chunk_bytes(lib, cache, store, chunk):
+    if chunk is None:
+        return workspace_bytes(cache, store)
+    lo, hi = chunk
+    p = _chunk_params(cache, lo, hi)
+    host = None
+    if cache.cu_seqlens is not None:
+        host = (cache.cu_host[lo:hi + 1] - cache.cu_host[lo]).to(torch.int32).contiguous()
+    return int(lib.sb_bwd_workspace_bytes(ctypes.byref(p), None if host is None else
+                                          ctypes.c_void_p(host.data_ptr()), int(store)))
 
 
 def _varlen_tiles(cache):
@@ -500,9 +515,7 @@ def _backward_call(lib, cache, d_o, ro, dq, dk, dv, store, phases, chunk, worksp
             fkb_off = units0 * nb
     qv, kv, vv, dov, dqv, dkv, dvv = views
     host = None if cu_host is None else ctypes.c_void_p(cu_host.data_ptr())
-    nbytes = int(lib.sb_bwd_workspace_bytes(ctypes.byref(p), host, int(store)))
-    ws = workspace if workspace is not None else torch.empty(nbytes, device=q.device,
-                                                             dtype=torch.uint8)
+    ws = workspace
     # the state pointer keeps its 64-float header in front of the chunk's rows (sb_bwd
     # reads only the rows): offset by 2 floats per row
     st_ptr = ctypes.c_void_p(state.data_ptr() + 8 * st_off)

@@ -36,8 +36,10 @@ import paper_2410_17980_b200 as sb  # noqa: E402
 from tests.gpu_util import make_qkv, to64  # noqa: E402
 
 
-def timed(fn, n=3):
-    fn()
+def timed(fn, n=5, warm=3):
+    # several warm-up calls: the first launches of a kernel on new inputs run slow
+    for _ in range(warm):
+        fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()

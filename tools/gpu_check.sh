@@ -11,3 +11,5 @@ for t in memcheck racecheck synccheck; do
 done
 tail -c 2500 gpurun_out/bench.log
 tail -40 gpurun_out/pytest_gpu.log
+timeout 900 python tests/reports/c3_skip_report.py --check-heads 0 --out gpurun_out/c3_skip.json > gpurun_out/c3_skip.log 2>&1
+tail -c 600 gpurun_out/c3_skip.log
