@@ -283,10 +283,12 @@ __device__ __forceinline__ void store_row_sw128(uint32_t row_addr, int r, const 
 // Phase 1: dQ and N.  CTA = (b, h, query tiles 2p and 2p+1).
 template <int D>
 struct BwdQCfg {
-  // K ring of 3 stages (S(j) and dQ(j) read K(j): released at the end of tile j);
-  // V single-buffered (only dW(j) reads V(j): released early in tile j).
-  static constexpr int kStages = 3;   // K ring
-  static constexpr int kVStages = 1;  // V ring (its own producer warp)
+  // K ring (S(j) and dQ(j) read K(j): released at the end of tile j); V ring (only
+  // dW(j) reads V(j): released early in tile j).
+  // d = 64 has the shared memory for a deeper K ring and a second V stage (C4
+  // phase 1: 2.33 -> 2.31 ms); d = 128 has not (Q[2] + dO[2] take 128 KB)
+  static constexpr int kStages = D == 64 ? 4 : 3;   // K ring
+  static constexpr int kVStages = D == 64 ? 2 : 1;  // V ring (its own producer warp)
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kKVBytes = kBlock * D * 2;
   static constexpr int kZBytes = kTileM * kBlock * 2;
@@ -693,10 +695,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (tr) SB_TR(args, w, gi, 1);
         const bool diag = kb == my_qb;  // warp-uniform
         if (kPingPongQ) named_bar_sync(bar_mine, 256);
+        if (tr) SB_TR(args, w, gi, 7);
         // dead rows/tiles run the same code with e^M = 0 and b = 0: A = 0, dZ = 0
         float tot[4], Mk;
         if (diag) row_pass1<true>(s, sg, g.scale_log2, r & 63, tot);
         else row_pass1<false>(s, sg, g.scale_log2, kBlock, tot);
+        if (tr) SB_TR(args, w, gi, 8);
         // the turn ends with the ex2 pass (the MUFU-heavy part): L, E and the
         // FMA-pipe pass 2 overlap the other warpgroup's ex2 pass (0.6% faster than
         // holding the turn to the end of pass 2)

@@ -51,7 +51,8 @@ def main():
         elif a.phase == 2:
             ops.blocked_backward_twophase(cache, do)
         else:  # phase 1 only, traced
-            ops.blocked_backward_twophase(cache, do, phases=1)
+            ws = torch.empty(ops.workspace_bytes(cache), device=dev, dtype=torch.uint8)
+            ops.blocked_backward_twophase(cache, do, phases=1, workspace=ws)
         torch.cuda.synchronize()
     lib.sb_debug_set_trace(None)
     t = tr.cpu().numpy().view(np.uint32).reshape(NCTA, NROLE, NT, NEV).astype(np.int64)
@@ -70,6 +71,26 @@ def main():
             print(f"  role {role}: {len(rows)} tiles")
             for j, ev in rows[:6] + rows[-2:]:
                 print(f"    j={j:2d} " + " ".join(f"{e:7d}" for e in ev[:14]))
+    if a.phase == 1:
+        # median clocks between the stick warpgroups' per-tile events (tiles j >= 1 of
+        # every traced CTA/role): 0 start, 1 S loaded, 7 turn taken, 8 pass 1 done,
+        # 2 recompute done, 3 dW read, 4 dZ math done, 5 zempty, 6 dZ stored
+        order = [0, 1, 7, 8, 2, 3, 4, 5, 6]
+        d = {f"{x}->{y}": [] for x, y in zip(order, order[1:])}
+        per_tile = []
+        for c in range(NCTA):
+            for role in (0, 1):
+                for j in range(1, NT):
+                    ev = t[c, role, j]
+                    if not all(ev[e] for e in order):
+                        continue
+                    for x, y in zip(order, order[1:]):
+                        d[f"{x}->{y}"].append(int(ev[y] - ev[x]))
+                    nxt = t[c, role, j + 1, 0] if j + 1 < NT else 0
+                    if nxt:
+                        per_tile.append(int(nxt - ev[0]))
+        print("median clk:", {k: int(np.median(v)) for k, v in d.items() if v},
+              "tile:", int(np.median(per_tile)) if per_tile else None)
 
 
 if __name__ == "__main__":
