@@ -17,9 +17,11 @@ roofline = the dominant kernel's algorithmic tensor FLOPs per launch / its CUDA-
           duration, against MEASURED_PEAKS.json bf16: the burst peak when the run held
           its SM clock at max without a power cap, else the sustained one (both
           fractions are reported).
-cpu_baseline = the CPU oracle port (oracle/, C, float32, all host threads) on a bounded
-          sample of the same workload (rank 0, N=1 only).
---impl reference times that CPU port as the reference arm (no GPU work).
+cpu_baseline = the reference's own CPU path (baseline/_ref: its NumPy blocked_forward +
+          blocked_backward_twophase, float32, one unit per host core) on a bounded sample
+          of the same workload (rank 0, N=1 only); the C port in oracle/ when the
+          reference is not installed.
+--impl reference times that CPU path as the reference arm (no GPU work).
 """
 
 from __future__ import annotations
@@ -132,33 +134,117 @@ def cpu_sample(n_units=None, threads=None):
             "seconds_per_unit": dt / n_units}
 
 
-def run_reference(args, rank, world):
-    """Reference arm: the reference's CPU algorithm (oracle C port) on the host cores.
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-    One step = one bounded sample of C2: as many (b, h) units as host threads, each
-    unit a full L=4096 d=128 fwd + two-phase bwd in f32.  value = tokens/s of that
-    sample (units are independent and equal-cost, so it is the whole-batch rate);
-    ms_per_step is the sample's measured wall time (not extrapolated)."""
+
+def _ref_unit(seed):
+    """One C2 (b, h) unit through the UNMODIFIED reference (baseline/_ref, installed from
+    /root/reference/pkg): blocked_forward(two_phase=True) + blocked_backward_twophase in
+    float32, its own NumPy code (blocked.py:129-206, :299-392).  Returns seconds."""
+    from sbattn import blocked as bl
+    rng = np.random.default_rng(seed)
+    q, k, v, w = (rng.standard_normal((L, D)).astype(np.float32) for _ in range(4))
+    lay = bl.plan_blocks(L)
+    t0 = time.perf_counter()
+    _, acc, st = bl.blocked_forward(q, k, v, lay, two_phase=True, dtype=np.float32)
+    bl.blocked_backward_twophase(bl.make_cache(q, k, v, lay, acc, st), w, lay)
+    return time.perf_counter() - t0
+
+
+def _ref_init():
+    sys.path.insert(0, REF_DIR)
+
+
+class RefSampler:
+    """The reference's own CPU path on all host cores: one unit per worker process
+    (spawned, one BLAS thread each: the reference's own threading is slower than serial,
+    SURVEY.md §8(a) `_map_ordered`).  None when baseline/_ref is not installed."""
+
+    def __init__(self):
+        self.pool = None
+        if not os.path.isdir(os.path.join(REF_DIR, "sbattn")):
+            return
+        import multiprocessing as mp
+        self.procs = os.cpu_count() or 1
+        old = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS")}
+        os.environ["OPENBLAS_NUM_THREADS"] = os.environ["OMP_NUM_THREADS"] = "1"
+        try:
+            self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_ref_init)
+            self.pool.map(_ref_init_probe, range(self.procs))  # workers up, sbattn imported
+        except Exception:
+            self.pool = None
+        for k_, v_ in old.items():
+            if v_ is None:
+                os.environ.pop(k_, None)
+            else:
+                os.environ[k_] = v_
+
+    def sample(self, n_units=None):
+        n_units = max(1, min(n_units or self.procs, B * H))
+        t0 = time.perf_counter()
+        per = self.pool.map(_ref_unit, range(n_units))
+        dt = time.perf_counter() - t0
+        t_full = dt * (B * H) / n_units
+        return {"value": B * L / t_full, "unit": UNIT, "cores": self.procs, "kind": "reference",
+                "sample": f"{n_units} of {B * H} (b,h) units of C2 (L=4096, d=128) through the "
+                          f"reference's own blocked_forward(two_phase=True) + "
+                          f"blocked_backward_twophase (NumPy, float32; baseline/_ref), one unit "
+                          f"per process on {self.procs} host cores, {dt:.1f}s wall "
+                          f"({statistics.median(per):.2f}s per unit); scaled linearly to the "
+                          f"full batch", "seconds": dt}
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.terminate()
+
+
+def _ref_init_probe(_):
+    from sbattn import blocked  # noqa: F401
+    return 0
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the reference's own CPU implementation of the path on the host cores
+    (baseline/_ref: its NumPy blocked_forward + blocked_backward_twophase), or the C port of
+    it in oracle/ when the reference is not installed.
+
+    One step = one bounded sample of C2: as many (b, h) units as host cores, each unit a
+    full L=4096 d=128 fwd + two-phase bwd in f32.  value = tokens/s of that sample (units are
+    independent and equal-cost, so it is the whole-batch rate); ms_per_step is the sample's
+    measured wall time (not extrapolated)."""
     if rank != 0:
         return
-    import oracle
-    oracle.build()
-    threads = oracle.n_threads_default()
-    units = max(1, min(args.cpu_units or threads, B * H))
+    ref = RefSampler()
+    if ref.pool is not None:
+        def one():
+            r = ref.sample(args.cpu_units or None)
+            return r, r["seconds"]
+        threads = ref.procs
+        units = max(1, min(args.cpu_units or threads, B * H))
+    else:
+        import oracle
+        oracle.build()
+        threads = oracle.n_threads_default()
+        units = max(1, min(args.cpu_units or threads, B * H))
+
+        def one():
+            r = cpu_sample(units, threads)
+            return r, r["seconds_per_unit"] * units
     t_all = time.perf_counter()
     for _ in range(max(1, args.warmup)):  # same-size samples, untimed
-        cpu_sample(units, threads)
+        one()
         if time.perf_counter() - t_all > 60:
             break
     n_warm = _ + 1
     vals, secs = [], []
     t_all = time.perf_counter()
     for _ in range(max(1, args.steps)):
-        s = cpu_sample(units, threads)
+        s, sec = one()
         vals.append(s["value"])
-        secs.append(s["seconds_per_unit"] * units)
+        secs.append(sec)
         if time.perf_counter() - t_all > 150:
             break
+    ref.close()
     value = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": len(vals), "warmup": n_warm, "ms_per_step": statistics.median(secs) * 1e3,
@@ -167,7 +253,7 @@ def run_reference(args, rank, world):
             "config": {"workload": WORKLOAD + " (CPU)",
                        "step": f"one sample of {units} of the {B * H} (b,h) units, one per host "
                                f"thread; tokens/s = units/{B * H} x {B * L} tokens / sample time"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": s["kind"],
                              "sample": s["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -439,7 +525,16 @@ def main():
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         try:
-            cpu = cpu_sample(args.cpu_units or None)
+            ref = RefSampler()
+            if ref.pool is not None:
+                ref.sample(args.cpu_units or None)  # warm-up sample
+                cpu = ref.sample(args.cpu_units or None)
+                cpu.pop("seconds")
+                ref.close()
+                port = cpu_sample(args.cpu_units or None)
+                cpu["port_value"] = port["value"]  # the C port of the same algorithm, for scale
+            else:
+                cpu = cpu_sample(args.cpu_units or None)
         except Exception as ex:
             cpu = {"error": repr(ex)}
 

@@ -41,8 +41,8 @@ SCHED_HEADER = 64  # floats at the start of the state / snapshot arrays (work-qu
 # The backward's workspace (M snapshots + the store mode's dZ tiles: phase 1 writes them,
 # phase 2 reads them instead of recomputing dO.V^T and dZ; bit-identical results) is bounded
 # by this many bytes per call: a larger problem runs in chunks of whole (b, h) units (C2:
-# 2.2 GB in one call; C3 at L=32768 would need 33 GB and runs in ~10 chunks).
-WORKSPACE_MAX_BYTES = int(float(os.environ.get("SB_WORKSPACE_MAX_GB", "4")) * 2**30)
+# 2.2 GB and C4 4.2 GB in one call; C3 at L=32768 would need 34 GB and runs in 5 chunks).
+WORKSPACE_MAX_BYTES = int(float(os.environ.get("SB_WORKSPACE_MAX_GB", "8")) * 2**30)
 SKIP_EPS_BF16 = 1e-6  # the reference's f32 default (blocked.py:43) is used for bf16
 
 
@@ -333,11 +333,15 @@ def workspace_bytes(cache: BlockedCache, store: bool = True) -> int:
 
 def workspace_cap_bytes(device=None) -> int:
     """Largest backward workspace one call allocates: the SB_WORKSPACE_MAX_GB cap
-    (default 4 GiB), and at most a quarter of the device memory free right now.
+    (default 8 GiB), and at most a quarter of the device memory free to this process.
     A larger problem runs in chunks of whole (b, h) units."""
     cap = WORKSPACE_MAX_BYTES
     try:
+        # free to this process: the driver's free memory plus what torch's caching
+        # allocator holds unused (mem_get_info alone counts that cache as taken, and a
+        # cap shrinking with it splits small problems into slow chunks)
         free, _ = torch.cuda.mem_get_info(device)
+        free += torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
         cap = min(cap, free // 4)
     except Exception:  # pragma: no cover - no device query possible
         pass
