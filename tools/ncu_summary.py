@@ -9,7 +9,7 @@ import subprocess
 import sys
 
 METRICS = [
-    ("ms", "gpu__time_duration.sum", 1.0),
+    ("us", "gpu__time_duration.sum", 1.0),
     ("regs", "launch__registers_per_thread", 1.0),
     ("issue %", "smsp__issue_active.avg.pct_of_peak_sustained_active", 1.0),
     ("tensor %", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
