@@ -7,6 +7,7 @@ BlockLayout / plan_blocks, plus the (b, h) sharding helper of dist.py.
 import pytest
 
 import paper_2410_17980_b200 as sb
+from paper_2410_17980_b200 import ops
 from paper_2410_17980_b200 import dist
 
 
@@ -62,3 +63,44 @@ def test_dense_layout_check():
     blhd = torch.zeros(2, 5, 4, 64).transpose(1, 2)
     assert _dense(blhd) and _same_layout(blhd, blhd, blhd)[0].stride() == blhd.stride()
     assert _dense(torch.zeros(1, 1, 7, 64)[:, :, :, :])
+
+
+def _cache(shape, cu=None):
+    import torch
+    q = torch.zeros(*shape, dtype=torch.bfloat16)
+    if cu is None:
+        lay = ops.plan_blocks(shape[2])
+        return ops.BlockedCache(q, q, q, 0.125, lay, None, None, None, False, 1e-6)
+    cu_host = torch.tensor(cu, dtype=torch.int32)
+    return ops.BlockedCache(q, q, q, 0.125, None, None, None, None, False, 1e-6,
+                            cu_seqlens=cu_host, max_seqlen=int((cu_host[1:] - cu_host[:-1]).max()),
+                            cu_host=cu_host)
+
+
+def test_backward_chunks_cover_units_under_the_cap():
+    """_unit_chunks (the workspace-capped backward's plan): contiguous ranges covering the
+    axis (batch entries, heads when B == 1, sequences for varlen), each within the cap
+    unless it is a single unit, fewest chunks (greedy maximal prefixes)."""
+    import ctypes
+    lib = ops._lib.load()
+    for shape in ((3, 2, 700, 64), (1, 5, 700, 128), (4, 1, 4096, 128)):
+        c = _cache(shape)
+        whole = ops.workspace_bytes(c)
+        axis = shape[0] if shape[0] > 1 else shape[1]
+        one = whole // axis
+        for cap in (whole, whole - 1, 2 * one + one // 2, one, 1):
+            ch = list(ops._unit_chunks(c, True, cap))
+            assert ch[0][0] == 0 and ch[-1][1] == axis
+            assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+            for lo, hi in ch:
+                p = ops._chunk_params(c, lo, hi)
+                need = lib.sb_bwd_workspace_bytes(ctypes.byref(p), None, 1)
+                assert need <= cap or hi - lo == 1
+            if cap >= whole:
+                assert ch == [(0, axis)]
+    lens = [300, 0, 700, 129, 64]
+    cu = [0] + list(__import__("itertools").accumulate(lens))
+    c = _cache((cu[-1], 2, 64), cu)
+    whole = ops.workspace_bytes(c)
+    ch = list(ops._unit_chunks(c, True, whole // 3))
+    assert len(ch) > 1 and ch[0][0] == 0 and ch[-1][1] == len(lens)
