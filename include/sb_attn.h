@@ -65,8 +65,9 @@ enum {
  * Packed variable-length batches (cu_seqlens != NULL): the tensors are
  * (total_tokens, H, d) with token stride stride_l and head stride stride_h
  * (stride_b unused); sequence b is tokens cu_seqlens[b] .. cu_seqlens[b+1]-1
- * (cu_seqlens: DEVICE int32 [batch+1], cu_seqlens[0] = 0); seqlen is the
- * longest sequence (grid sizing).  Every sequence is an independent problem
+ * (cu_seqlens: DEVICE int32 [batch+1], cu_seqlens[0] = 0); seqlen must be at least
+ * the longest sequence (work items are counted from it: sb_bwd checks it against the
+ * host offsets, sb_fwd cannot).  Every sequence is an independent problem
  * whose 64-blocks start at its first token.  Per-row outputs (log_rem,
  * row_offset) are then (total_tokens, H); first_kb and M/N are packed sequence
  * by sequence, head-major (sizes: sb_varlen_elems). */

@@ -242,6 +242,14 @@ int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, co
       !aligned16(dk) || !aligned16(dv) || !aligned16(state) ||
       (reinterpret_cast<uintptr_t>(workspace) & 127))
     return SB_ERR_UNSUPPORTED;
+  if (p->cu_seqlens) {
+    // the host offsets must describe the batch the kernels see: every sequence within
+    // seqlen (item counts come from it) and the last offset at total_tokens
+    if (cu_seqlens_host[0] != 0 || cu_seqlens_host[p->batch] != p->total_tokens)
+      return SB_ERR_SHAPE;
+    for (int b = 0; b < p->batch; ++b)
+      if (cu_seqlens_host[b + 1] - cu_seqlens_host[b] > p->seqlen) return SB_ERR_SHAPE;
+  }
   const size_t need = sb_bwd_workspace_bytes(p, cu_seqlens_host, store);
   if (need == 0 || workspace_bytes < need) return SB_ERR_SHAPE;
   const int64_t m = snapshot_floats(p, cu_seqlens_host), mb = round_up(m * 4);

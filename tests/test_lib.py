@@ -179,3 +179,17 @@ def test_workspace_checked(lib):
     p.cu_seqlens = ctypes.cast(cu, ctypes.c_void_p)
     p.total_tokens = 256
     assert _bwd(lib, p, d, ctypes.c_void_p(1024), 1 << 30) == 5
+
+
+def test_varlen_offsets_checked_by_the_backward(lib):
+    """A seqlen below the longest sequence would drop work items silently; the
+    backward checks the host offsets against it (and total_tokens)."""
+    p = _params(B=2, H=2, L=128)
+    cu = (ctypes.c_int32 * 3)(0, 64, 200)  # second sequence 136 > seqlen 128
+    p.cu_seqlens = ctypes.cast(cu, ctypes.c_void_p)
+    p.total_tokens = 200
+    d = ctypes.c_void_p(16)
+    assert _bwd(lib, p, d, ctypes.c_void_p(1024), 1 << 40, cu_host=cu) == 1
+    p.seqlen = 136
+    p.total_tokens = 199  # last offset must be total_tokens
+    assert _bwd(lib, p, d, ctypes.c_void_p(1024), 1 << 40, cu_host=cu) == 1
