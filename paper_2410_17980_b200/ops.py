@@ -333,19 +333,26 @@ def workspace_bytes(cache: BlockedCache, store: bool = True) -> int:
 
 def workspace_cap_bytes(device=None) -> int:
     """Largest backward workspace one call allocates: the SB_WORKSPACE_MAX_GB cap
-    (default 8 GiB), and at most a quarter of the device memory free to this process.
-    A larger problem runs in chunks of whole (b, h) units."""
+    (default 8 GiB) and at most 1/16 of the device memory.  A larger problem runs in
+    chunks of whole (b, h) units.  (No free-memory query: cudaMemGetInfo waits for the
+    device, ~10 ms per backward call on a busy GPU.)"""
     cap = WORKSPACE_MAX_BYTES
     try:
-        # free to this process: the driver's free memory plus what torch's caching
-        # allocator holds unused (mem_get_info alone counts that cache as taken, and a
-        # cap shrinking with it splits small problems into slow chunks)
-        free, _ = torch.cuda.mem_get_info(device)
-        free += torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
-        cap = min(cap, free // 4)
+        cap = min(cap, _device_total_bytes(torch.device("cuda", torch.cuda.current_device())
+                                           if device is None else torch.device(device)) // 16)
     except Exception:  # pragma: no cover - no device query possible
         pass
     return cap
+
+
+_TOTAL = {}
+
+
+def _device_total_bytes(device) -> int:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _TOTAL:
+        _TOTAL[idx] = torch.cuda.get_device_properties(idx).total_memory
+    return _TOTAL[idx]
 
 
 def _unit_chunks(cache: BlockedCache, store: bool, cap: int):
