@@ -151,6 +151,29 @@ def _ref_unit(seed):
     return time.perf_counter() - t0
 
 
+def _ref_unit_fused(seed):
+    """The same unit through blocked_forward(two_phase=False) + blocked_backward_fused, the
+    variant the reference's own `sb bench` times (cli.py:433-438).  Returns seconds."""
+    from sbattn import blocked as bl
+    rng = np.random.default_rng(seed)
+    q, k, v, w = (rng.standard_normal((L, D)).astype(np.float32) for _ in range(4))
+    lay = bl.plan_blocks(L)
+    t0 = time.perf_counter()
+    _, acc, st = bl.blocked_forward(q, k, v, lay, dtype=np.float32)
+    bl.blocked_backward_fused(bl.make_cache(q, k, v, lay, acc, st), w, lay)
+    return time.perf_counter() - t0
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def _ref_init():
     sys.path.insert(0, REF_DIR)
 
@@ -179,13 +202,16 @@ class RefSampler:
             else:
                 os.environ[k_] = v_
 
-    def sample(self, n_units=None):
+    def sample(self, n_units=None, fused=False):
         n_units = max(1, min(n_units or self.procs, B * H))
         t0 = time.perf_counter()
-        per = self.pool.map(_ref_unit, range(n_units))
+        per = self.pool.map(_ref_unit_fused if fused else _ref_unit, range(n_units))
         dt = time.perf_counter() - t0
         t_full = dt * (B * H) / n_units
+        if fused:
+            return {"value": B * L / t_full, "seconds": dt}
         return {"value": B * L / t_full, "unit": UNIT, "cores": self.procs, "kind": "reference",
+                "cpu": _cpu_model(),
                 "sample": f"{n_units} of {B * H} (b,h) units of C2 (L=4096, d=128) through the "
                           f"reference's own blocked_forward(two_phase=True) + "
                           f"blocked_backward_twophase (NumPy, float32; baseline/_ref), one unit "
@@ -407,9 +433,29 @@ def main():
                 "step_frac_sustained": tflops / world / sustained}
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            roofline["traffic"] = json.load(f).get(dom)
+            traffic = json.load(f)
+        roofline["traffic"] = traffic.get(dom)
+        # achieved DRAM rate per kernel: ncu bytes per launch (profiles/traffic.json, the
+        # M snapshot and dZ tile round trip included) over this run's kernel time
+        roofline["hbm_gbs_per_kernel"] = {n: round(traffic[n] / (v[0] / 1e3) / 1e9, 1)
+                                          for n, v in kernels.items() if n in traffic}
     except Exception:
         pass
+    # Secondary bound: the special-function unit.  MUFU operations per
+    # score element from the kernels' SASS (per 64-column row of a tile: forward 65 ex2 +
+    # 4 rcp + 2 lg2; phase 1 65 ex2 + 4 rcp + 2 lg2; phase 2 65 ex2 + 4 rcp), elements per
+    # pass = tiles x 64 x 64 (diagonal tiles whole), at 16 per clock per SM.
+    elems = B * H * (L // 64) * (L // 64 + 1) // 2 * 4096
+    mufu = {"sb_fwd_pp_kernel": 71 / 64, "sb_bwd_q_kernel": 71 / 64, "sb_bwd_kvs_kernel": 69 / 64}
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    mufu_rate = 16 * sm_count * mhz * 1e6  # ops/s
+    roofline["sfu"] = {
+        "unit": "MUFU ops/s", "peak": mufu_rate,
+        "per_kernel_frac": {n: round(mufu[n] * elems / (kernels[n][0] / 1e3) / mufu_rate, 3)
+                            for n in kernels if n in mufu},
+        "step_floor_ms": sum(mufu.values()) * elems / mufu_rate * 1e3,
+        "note": "16 MUFU ops/clk/SM at the run's median SM clock; ops per element from SASS"}
 
     # ---------------------------------------------------------------- e2e
     e2e = None
@@ -542,6 +588,8 @@ def main():
                 ref.sample(args.cpu_units or None)  # warm-up sample
                 cpu = ref.sample(args.cpu_units or None)
                 cpu.pop("seconds")
+                # the fused-backward variant the reference's `sb bench` times, for scale
+                cpu["fused_value"] = ref.sample(args.cpu_units or None, fused=True)["value"]
                 ref.close()
                 port = cpu_sample(args.cpu_units or None)
                 cpu["port_value"] = port["value"]  # the C port of the same algorithm, for scale
