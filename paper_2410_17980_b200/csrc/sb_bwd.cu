@@ -69,6 +69,7 @@ __device__ __forceinline__ void row_pass1(float* s, float* sg, float scale_log2,
   // the scale on adjacent column pairs, everything else on the group pairs
   // (0,1) and (2,3), i.e. columns (c, c+16); bit-identical to the scalar form.
   const float2 sl2 = make_float2(scale_log2, scale_log2);
+  float2 tp[2] = {make_float2(1.0f, 1.0f), make_float2(1.0f, 1.0f)};
 #pragma unroll
   for (int c = 0; c < kBlock; c += 2) {
     const float2 z = mul2(make_float2(s[c], s[c + 1]), sl2);
@@ -80,7 +81,6 @@ __device__ __forceinline__ void row_pass1(float* s, float* sg, float scale_log2,
     s[c] = t0;
     s[c + 1] = t1;
   }
-  float2 tp[2] = {make_float2(1.0f, 1.0f), make_float2(1.0f, 1.0f)};
 #pragma unroll
   for (int i = 0; i < 16; ++i)
 #pragma unroll
@@ -193,10 +193,11 @@ __device__ __forceinline__ void recompute_row(float* s, float* sg, float scale_l
 // group (softplus2 of Z = lg2 t; where t = inf, z itself from the q row and the key
 // rows in global memory).  Out of line with t[] in local memory, so the hot
 // path's code and registers stay as they were.
-__device__ __noinline__ float row_lt_total_slow(const float* t, const float* tot,
+__device__ __noinline__ float row_lt_total_slow(const float* t, float4 tot4,
                                                 const __nv_bfloat16* qrow,
                                                 const __nv_bfloat16* krow0, int64_t ld, int d,
                                                 float scale_log2) {
+  const float tot[4] = {tot4.x, tot4.y, tot4.z, tot4.w};
   float lg[4];
   for (int g = 0; g < 4; ++g) {
     if (tot[g] < kBatchedWide) {
@@ -714,7 +715,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             float tl[kBlock];  // local-memory copy for the out-of-line rare path
 #pragma unroll
             for (int c = 0; c < kBlock; ++c) tl[c] = s[c];
-            L = row_lt_total_slow(tl, tot, args.q + u.out_off + (int64_t)row * g.sl,
+            L = row_lt_total_slow(tl, make_float4(tot[0], tot[1], tot[2], tot[3]),
+                                  args.q + u.out_off + (int64_t)row * g.sl,
                                   args.k + u.out_off + (int64_t)kb * kBlock * g.sl, g.sl, D,
                                   g.scale_log2);
           }
