@@ -564,6 +564,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         issue_w(0);
         for (int j = 0; j < n_w; ++j) {
           if (j + 1 < n_w) issue_s(j + 1);
+          // d=64 (K ring 4, V ring 2): dW(j+1) ahead of dQ(j), as soon as dW(j) was read
+          // (C4 phase 1 2.32 -> 2.30 ms); d=128 (K ring 3, one V buffer): after dQ(j),
+          // whose commit frees the K slot (the early order measured 0.915 -> 0.956 ms)
+          constexpr bool kEarlyW = D == 64;
+          if (kEarlyW && j + 1 < n_w) issue_w(j + 1);
           const int js = jg + j, s = js % ST, gi = ig + j;
           mbar_wait(zfull, gi & 1);
           SB_TR(args, 2 + w, gi, 11);
@@ -585,7 +590,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
           }
           __syncwarp();
-          if (j + 1 < n_w) issue_w(j + 1);
+          if (!kEarlyW && j + 1 < n_w) issue_w(j + 1);
           if (kStoreZ) {  // the store has read the buffer: second arrival on zempty
             if (leader) {
               bulk_wait_read0();
