@@ -19,8 +19,15 @@ if "--many" in sys.argv:
     # >= 3 items per CTA in every kernel (512 forward / phase-1 items, 1024 phase-2
     # items over 148 CTAs): the cross-item barrier phases and the work-queue ring wrap
     CASES = [(4, 64, 512, 64, False), (4, 64, 512, 128, True)]
+if "--many" in sys.argv:
+    # partial skipping (mu = -6 shifted logits): the skip-on forward's vote words, stops
+    # mid-stream and the producer's ring release after a stop
+    CASES.append((2, 16, 1024, 128, "shift"))
 for (B, H, L, d, skip) in CASES:
-    q, k, v, do = make_qkv(B, H, L, d, seed=1)
+    fam = "random"
+    if skip == "shift":
+        fam, skip = "shift", True
+    q, k, v, do = make_qkv(B, H, L, d, seed=1, family=fam, mu=-6.0)
     o, lr, st, cache = sb.blocked_forward(q, k, v, skip=skip)
     for store in (False, True):
         dq, dk, dv, _ = sb.blocked_backward_twophase(cache, do, store_tiles=store)
