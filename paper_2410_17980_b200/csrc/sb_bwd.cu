@@ -299,7 +299,7 @@ struct BwdQCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kVStages * kKVBytes;  // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 2 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8;
+  static constexpr int kNumBars = 2 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8 + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -372,10 +372,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), bar_qdofree + 1,
                      bar_qdofree + 5};
+  uint64_t* bar_qtm = bar_qdofree + 9;  // [2] the warpgroup copied its Q tile into TMEM
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qdo, 1);
     mbar_init(bar_qdo + 1, 1);
+    mbar_init(bar_qtm, 128);
+    mbar_init(bar_qtm + 1, 128);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_kfull + s, 1);
       mbar_init(bar_kempty + s, 2);  // one arrival per warpgroup issuer (dQ read K)
@@ -487,13 +490,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                *dq_free = sfull + 7;
       constexpr uint32_t idesc_s = idesc_bf16(128, 64, 0, 0);  // Q K^T, dO V^T
       constexpr uint32_t idesc_q = idesc_bf16(128, D, 0, 1);   // dZ K: K is MN-major
-      const uint64_t dq = sdesc_sw128(smem_u32(smem + C::kOffQ + w * C::kQBytes), 16, 1024);
       const uint64_t ddo = sdesc_sw128(smem_u32(smem + C::kOffDO + w * C::kQBytes), 16, 1024);
       const uint64_t dk = sdesc_sw128(smem_u32(smem + C::kOffK), 16, 1024);
       const uint64_t dkmn = sdesc_sw128(smem_u32(smem + C::kOffK), kBlock * 128, 1024);
       const uint64_t dv = sdesc_sw128(smem_u32(smem + C::kOffV), 16, 1024);
       const uint64_t dz = sdesc_sw128(smem_u32(smem + C::kOffZ + w * C::kZBytes), 16, 1024);
-      const uint32_t tS = tbase + w * 256, tW = tS + 64, tQ = tS + 128;
+      // per warpgroup: dQ accumulator (128 columns), one buffer for S and then dW (64),
+      // Q (the TS MMA's A operand, 64)
+      const uint32_t tQ = tbase + w * 256, tS = tQ + 128, tW = tS, tQtm = tQ + 192;
       const bool leader = elect_one();
       int jg = 0, ni = 0, ig = 0, nwi = 0;
       for (int kq = 0;; ++kq) {
@@ -527,15 +531,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int js = jg + j, s = js % ST, gi = ig + j;
           mbar_wait(bar_kfull + s, (js / ST) & 1);
           SB_TR(args, 2 + w, gi, 13);
-          if (gi >= 1) mbar_wait(sempty, (gi - 1) & 1);
+          // the shared S/dW buffer is free once dW(j-1) was read; the item's first S
+          // needs this item's Q in TMEM
+          if (gi >= 1) mbar_wait(wempty, (gi - 1) & 1);
+          if (j == 0) mbar_wait(bar_qtm + w, nwi & 1);
           SB_TR(args, 2 + w, gi, 8);
           tc_fence_after();
           if (leader) {
 #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (k >> 2) * (kTileM * 128) + (k & 3) * 32;
               const uint32_t offk = (k >> 2) * (kBlock * 128) + (k & 3) * 32;
-              umma_ss_at(tS, dq, off, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
+              umma_ts_at(tS, tQtm + k * 8, dk, s * C::kKVBytes + offk, idesc_s, k > 0);
             }
             umma_commit(sfull);
           }
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         auto issue_w = [&](int j) {
           const int js = jg + j, gi = ig + j, sv = js % VST;
           mbar_wait(bar_vfull + sv, (js / VST) & 1);
-          if (gi >= 1) mbar_wait(wempty, (gi - 1) & 1);
+          mbar_wait(sempty, gi & 1);  // S(j) was read out of the shared buffer
           SB_TR(args, 2 + w, gi, 10);
           tc_fence_after();
           if (leader) {
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t tS = tbase + w * 256 + lane_base, tW = tS + 64, tQ = tS + 128;
+    const uint32_t tQ = tbase + w * 256 + lane_base, tS = tQ + 128, tW = tS, tQtm = tQ + 192;
     const uint32_t z_row = smem_u32(smem + C::kOffZ + w * C::kZBytes) + r * 128;
     const float scale = g.scale_log2 * kLn2;
     const bool tr = quarter == 0 && lane == 0;
@@ -684,6 +690,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         m_lo = (float)(a0 - (double)m_hi);
       }
       float bsum = 0.0f;  // running b (blocked.py:342, :354)
+      {
+        // copy this thread's Q row (TMA-swizzled smem) into TMEM lane r: the A operand of
+        // the TS MMA S = Q K^T (as the forward does)
+        mbar_wait(bar_qdo + w, nwi & 1);
+        const uint32_t qrow = smem_u32(smem + C::kOffQ + w * C::kQBytes) + r * 128;
+        uint32_t qv[D / 2];
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+          const uint4 x = ld_shared_v4(qrow + (c >> 3) * (kTileM * 128) + (((c & 7) ^ (r & 7)) << 4));
+          qv[4 * c] = x.x;
+          qv[4 * c + 1] = x.y;
+          qv[4 * c + 2] = x.z;
+          qv[4 * c + 3] = x.w;
+        }
+        if constexpr (D == 128) tmem_st64(tQtm, qv);
+        else tmem_st32(tQtm, qv);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar_qtm + w);
+      }
       if (tr) SB_TR(args, w, nwi, 11);
       for (int j = 0; j < n_w; ++j) {
         const int kb = it.kb_lo + j, gi = ig + j;
