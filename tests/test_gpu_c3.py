@@ -101,3 +101,25 @@ def test_long_rows_rollback_matches_oracle():
                                     / np.maximum(1.0, np.abs(ref["log_rem"]))))}
     print("long rows", {n: f"{e:.2e}" for n, e in errs.items()})
     assert max(errs.values()) < TOL
+
+
+def test_partial_skip_long_rows_grads_match_oracle():
+    """mu = -6 shifted logits at L = 16384, skip on (partial skipping: rows stop at
+    different key blocks): the skip-on forward's decisions, its compensated a (the
+    backward's state) and phase 1's M rollback over the visited tiles only; o, dq, dk, dv
+    vs the f64 oracle on two heads."""
+    import paper_2410_17980_b200 as sb
+    q, k, v, d_o = make_qkv(1, 2, 16384, 128, seed=29, family="shift", mu=-6.0)
+    o, log_rem, st, cache = sb.blocked_forward(q, k, v, skip=True, skip_eps=1e-6)
+    dq, dk, dv, _ = sb.blocked_backward_twophase(cache, d_o)
+    torch.cuda.synchronize()
+    ref = oracle.tiled_forward(to64(q[0]), to64(k[0]), to64(v[0]), block=64, skip=True,
+                               skip_eps=1e-6)
+    np.testing.assert_array_equal(st.first_kb[0].cpu().numpy(), ref["first_kb"])
+    assert 0.05 < 1.0 - st.visited / st.total < 0.95  # partial skipping
+    rdq, rdk, rdv, _ = oracle.tiled_backward(to64(q[0]), to64(k[0]), to64(v[0]), to64(d_o[0]),
+                                             ref, block=64)
+    errs = {"o": rel_to_max(to64(o[0]), ref["o"]), "dq": rel_to_max(to64(dq[0]), rdq),
+            "dk": rel_to_max(to64(dk[0]), rdk), "dv": rel_to_max(to64(dv[0]), rdv)}
+    print("partial skip", st.visited, "/", st.total, {n: f"{e:.2e}" for n, e in errs.items()})
+    assert max(errs.values()) < TOL
