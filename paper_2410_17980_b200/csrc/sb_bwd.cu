@@ -299,7 +299,7 @@ struct BwdQCfg {
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kVStages * kKVBytes;  // Z[2] (one per WG)
   static constexpr int kOffBar = kOffZ + 2 * kZBytes;
-  static constexpr int kNumBars = 2 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8 + 2;
+  static constexpr int kNumBars = 2 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8 + 2 + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
@@ -373,12 +373,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const SchedRing sq{reinterpret_cast<int*>(smem + C::kOffMisc + 16), bar_qdofree + 1,
                      bar_qdofree + 5};
   uint64_t* bar_qtm = bar_qdofree + 9;  // [2] the warpgroup copied its Q tile into TMEM
+  // Q and dO land on separate barriers (bar_qdo: Q only), Q first: the Q copy into TMEM
+  // and the item's first S do not wait for dO
+  uint64_t* bar_do = bar_qdofree + 11;  // [2]
 
   if (threadIdx.x == 0) {
     mbar_init(bar_qdo, 1);
     mbar_init(bar_qdo + 1, 1);
     mbar_init(bar_qtm, 128);
     mbar_init(bar_qtm + 1, 128);
+    mbar_init(bar_do, 1);
+    mbar_init(bar_do + 1, 1);
     for (int s = 0; s < ST; ++s) {
       mbar_init(bar_kfull + s, 1);
       mbar_init(bar_kempty + s, 2);  // one arrival per warpgroup issuer (dQ read K)
@@ -430,15 +435,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (leader) {
           const int nw = it.has1 ? 2 : 1;
           for (int w = 0; w < nw; ++w) {
-            mbar_expect_tx(bar_qdo + w, 2 * C::kQBytes);
-            for (int c = 0; c < D / 64; ++c) {
-              const int row0 = (2 * it.p + w) * kTileM;
+            mbar_expect_tx(bar_qdo + w, C::kQBytes);
+            for (int c = 0; c < D / 64; ++c)
               tma_load_4d(&tm_q, bar_qdo + w, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
-                          c * 64, u.trow0 + row0, it.h, u.tb);
-              tma_load_4d(&tm_do, bar_qdo + w,
+                          c * 64, u.trow0 + (2 * it.p + w) * kTileM, it.h, u.tb);
+          }
+          for (int w = 0; w < nw; ++w) {
+            mbar_expect_tx(bar_do + w, C::kQBytes);
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_4d(&tm_do, bar_do + w,
                           smem + C::kOffDO + w * C::kQBytes + c * (kTileM * 128), c * 64,
-                          u.trow0 + row0, it.h, u.tb);
-            }
+                          u.trow0 + (2 * it.p + w) * kTileM, it.h, u.tb);
           }
         }
         __syncwarp();
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           continue;
         }
         const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
-        mbar_wait(bar_qdo + w, nwi & 1);  // this warpgroup's nwi-th tile
+        mbar_wait(bar_do + w, nwi & 1);  // dO of this warpgroup's nwi-th tile (dW reads it)
         // Static issue order: S(j+1) once S(j) was read (it runs while the
         // warpgroup still works on tile j), dQ(j) once dZ(j) is in smem, dW(j+1)
         // once dW(j) was read and V(j+1) landed (V is single-buffered).
