@@ -26,6 +26,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// The tensor-map encoder is a driver call and needs a current context on the calling
+// thread.  A thread that has only run cached-allocator work (torch's autograd worker
+// calling the backward) may have the right current device but no context bound yet:
+// cudaSetDevice on the current device binds its primary context without changing it.
+int ensure_context() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaSetDevice(dev) != cudaSuccess)
+    return SB_ERR_DEVICE;
+  return SB_OK;
+}
+
 // 4-D map over (d, L, H, B) of a bf16 tensor; box = 64 columns x rows.
 int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
   auto fn = encode_fn();
@@ -50,6 +61,12 @@ int make_map(CUtensorMap* m, const void* ptr, const sb_params_t* p, int rows) {
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box,
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && std::getenv("SB_DEBUG"))
+    std::fprintf(stderr, "make_map: %d ptr %p dims %llu %llu %llu %llu strides %llu %llu %llu rows %d\n",
+                 (int)r, ptr, (unsigned long long)dims[0], (unsigned long long)dims[1],
+                 (unsigned long long)dims[2], (unsigned long long)dims[3],
+                 (unsigned long long)strides[0], (unsigned long long)strides[1],
+                 (unsigned long long)strides[2], rows);
   return r == CUDA_SUCCESS ? SB_OK : SB_ERR_LAUNCH;
 }
 
@@ -65,6 +82,8 @@ int make_tile_map(CUtensorMap* m, void* ptr, size_t bytes) {
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && std::getenv("SB_DEBUG"))
+    std::fprintf(stderr, "make_tile_map: %d ptr %p bytes %zu\n", (int)r, ptr, bytes);
   return r == CUDA_SUCCESS ? SB_OK : SB_ERR_LAUNCH;
 }
 
@@ -199,7 +218,7 @@ int sb_fwd(const sb_params_t* p, const void* q, const void* k, const void* v, vo
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return SB_ERR_UNSUPPORTED;
   if (state && !aligned16(state)) return SB_ERR_UNSUPPORTED;
   CUtensorMap tq, tk, tv;
-  if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tk, k, p, 64)) ||
+  if ((st = ensure_context()) || (st = make_map(&tq, q, p, 128)) || (st = make_map(&tk, k, p, 64)) ||
       (st = make_map(&tv, v, p, 64)))
     return st;
   sb::FwdArgs a;
@@ -255,7 +274,7 @@ int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, co
   const int64_t m = snapshot_floats(p, cu_seqlens_host), mb = round_up(m * 4);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   CUtensorMap tq, tdo, tk, tv, tz;
-  if ((st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
+  if ((st = ensure_context()) || (st = make_map(&tq, q, p, 128)) || (st = make_map(&tdo, d_o, p, 128)) ||
       (st = make_map(&tk, k, p, 64)) || (st = make_map(&tv, v, p, 64)))
     return st;
   std::memset(&tz, 0, sizeof(tz));
@@ -280,6 +299,8 @@ int sb_bwd(const sb_params_t* p, const void* q, const void* k, const void* v, co
   a.sched = reinterpret_cast<unsigned*>(ws);
   int rc = sb::bwd_dispatch(p->head_dim, tq, tdo, tk, tv, tz, a, phases, store != 0,
                             reinterpret_cast<cudaStream_t>(stream));
+  if (rc && std::getenv("SB_DEBUG"))
+    std::fprintf(stderr, "sb_bwd: dispatch error %d (%s)\n", rc, cudaGetErrorString((cudaError_t)rc));
   return rc ? SB_ERR_LAUNCH : SB_OK;
 }
 
