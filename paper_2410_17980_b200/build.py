@@ -37,7 +37,7 @@ LIB_TRACE = os.path.join(HERE, "libsbattn_trace.so")
 
 
 def build(force: bool = False, verbose: bool = False, trace: bool = False,
-          variant: str = "") -> str:
+          variant: str = "", defines: tuple = ()) -> str:
     """Compile libsbattn.so (or, with trace=True, the -DSB_TRACE tuning variant
     libsbattn_trace.so that records per-event SM clocks, tools/trace_kernels.py;
     variant="nomath" builds libsbattn_nomath.so, the pipeline without the stick
@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False,
         lib = os.path.join(HERE, f"libsbattn_{variant}.so")
         tag = "_" + variant
         extra = {"nomath": ["-DSB_NOMATH"], "trace_nomath": ["-DSB_NOMATH", "-DSB_TRACE"],
-                 "noz": ["-DSB_NOZ"], "nomath_noz": ["-DSB_NOMATH", "-DSB_NOZ"]}[variant]
+                 "noz": ["-DSB_NOZ"], "nomath_noz": ["-DSB_NOMATH", "-DSB_NOZ"]}.get(variant, [])
+        extra = extra + ["-D" + d for d in defines]  # tuning A/B builds (tools/ablate.py)
     if not force and not _stale(lib):
         return lib
     jobs = []

@@ -286,15 +286,25 @@ template <int D>
 struct BwdQCfg {
   // K ring (S(j) and dQ(j) read K(j): released at the end of tile j); V ring (only
   // dW(j) reads V(j): released early in tile j).
-  // d = 64 has the shared memory for a deeper K ring and a second V stage (C4
-  // phase 1: 2.33 -> 2.31 ms); d = 128 has not (Q[2] + dO[2] take 128 KB)
-  static constexpr int kStages = D == 64 ? 4 : 3;   // K ring
-  static constexpr int kVStages = D == 64 ? 2 : 1;  // V ring (its own producer warp)
+  // Q only stages the copy into TMEM at the item start: d = 128 keeps ONE Q buffer that
+  // the two warpgroups' tiles take in turn, which makes room for a second V stage and a
+  // fourth K stage (C2 phase 1 0.909 -> 0.896 ms with dW(j+1) issued ahead of dQ(j);
+  // V ring 2 alone 0.902); d = 64 has room for a Q buffer per warpgroup, a K ring of 4
+  // and the V ring (C4 phase 1: 2.33 -> 2.31 ms)
+#ifndef SB_P1_KST128
+#define SB_P1_KST128 4
+#endif
+#ifndef SB_P1_VST128
+#define SB_P1_VST128 2
+#endif
+  static constexpr int kStages = D == 64 ? 4 : SB_P1_KST128;   // K ring
+  static constexpr int kVStages = D == 64 ? 2 : SB_P1_VST128;  // V ring (its own producer warp)
+  static constexpr int kQBufs = D == 64 ? 2 : (SB_P1_VST128 > 1 ? 1 : 2);
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kKVBytes = kBlock * D * 2;
   static constexpr int kZBytes = kTileM * kBlock * 2;
-  static constexpr int kOffQ = 0;                       // Q[2]
-  static constexpr int kOffDO = kOffQ + 2 * kQBytes;    // dO[2]
+  static constexpr int kOffQ = 0;                          // Q[kQBufs]
+  static constexpr int kOffDO = kOffQ + kQBufs * kQBytes;  // dO[2]
   static constexpr int kOffK = kOffDO + 2 * kQBytes;    // K ring
   static constexpr int kOffV = kOffK + kStages * kKVBytes;
   static constexpr int kOffZ = kOffV + kVStages * kKVBytes;  // Z[2] (one per WG)
@@ -302,6 +312,8 @@ struct BwdQCfg {
   static constexpr int kNumBars = 2 + 2 * kStages + 2 * kVStages + 2 * 8 + 1 + 8 + 2 + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
+  static_assert(kSmem <= 232448, "exceeds the 227 KB opt-in shared memory per block");
+  __host__ __device__ static constexpr int q_off(int w) { return kOffQ + (kQBufs == 2 ? w : 0) * kQBytes; }
   static constexpr uint32_t kTmemCols = 512;  // per WG w at w*256: S +0, dW +64, dQ +128
 };
 
@@ -339,8 +351,9 @@ __device__ __forceinline__ QItem q_item(const Geom& g, const int* first_kb, int 
 
 // Persistent: one CTA per SM takes (unit, query pair) items from a global work
 // queue.  The K ring / V buffer and each warpgroup's S, dW, dZ barriers run on
-// counters that continue across items; the next item's Q/dO load once both
-// warpgroups issued their last dW of the current item (qdo_free), and its
+// counters that continue across items; the next item's Q[w] loads once warpgroup w
+// copied the current Q tile into TMEM (bar_qtm), its dO once both warpgroups issued
+// their last dW of the current item (qdo_free), and its
 // first dQ MMA waits until the warpgroup read dQ out of TMEM (dq_free).
 // kStoreZ (store mode): each dZ tile also goes to the tile workspace (TMA store
 // from the swizzled smem buffer, issued with the dQ MMA) for phase 2 to reuse.
@@ -423,23 +436,42 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
       }
-      int jg = 0, ni = 0;
+      int jg = 0, ni = 0, nq[2] = {0, 0}, qlast = -1;
       for (int kq = 0;; ++kq) {
         const int idx = sched_produce(sq, kq, args.sched, n_items);
         if (idx < 0) break;
         const QItem it = q_item(g, args.first_kb, idx, kStoreZ);
         if (!it.valid) continue;
         const Unit& u = it.u;
-        if (ni >= 1) mbar_wait(bar_qdofree, (ni - 1) & 1);
-        SB_TR(args, 0, ni, 12);
-        if (leader) {
-          const int nw = it.has1 ? 2 : 1;
-          for (int w = 0; w < nw; ++w) {
+        const int nw = it.has1 ? 2 : 1;
+        // A Q buffer is free as soon as the warpgroup whose tile it held copied it into
+        // TMEM (early in that item): the next Q loads while the current item still
+        // streams.  One shared buffer (d = 128): WG1's tile first (WG1 takes the first
+        // turn of every round), WG0's after WG1 copied it (L2-prefetched meanwhile).
+        for (int i = 0; i < nw; ++i) {
+          const int w = C::kQBufs == 2 ? i : nw - 1 - i;
+          const int prev = C::kQBufs == 2 ? w : qlast;
+#ifdef SB_QLATE64
+          if (C::kQBufs == 2 && ni >= 1) mbar_wait_warp(bar_qdofree, (ni - 1) & 1);
+#endif
+          if (prev >= 0 && nq[prev] >= 1) mbar_wait_warp(bar_qtm + prev, (nq[prev] - 1) & 1);
+          if (leader) {
             mbar_expect_tx(bar_qdo + w, C::kQBytes);
             for (int c = 0; c < D / 64; ++c)
-              tma_load_4d(&tm_q, bar_qdo + w, smem + C::kOffQ + w * C::kQBytes + c * (kTileM * 128),
-                          c * 64, u.trow0 + (2 * it.p + w) * kTileM, it.h, u.tb);
+              tma_load_4d(&tm_q, bar_qdo + w, smem + C::q_off(w) + c * (kTileM * 128), c * 64,
+                          u.trow0 + (2 * it.p + w) * kTileM, it.h, u.tb);
+            if (C::kQBufs == 1 && i == 0 && nw == 2)
+              for (int c = 0; c < D / 64; ++c)
+                tma_prefetch_4d(&tm_q, c * 64, u.trow0 + 2 * it.p * kTileM, it.h, u.tb);
           }
+          __syncwarp();
+          ++nq[w];
+          qlast = w;
+        }
+        // dO: once both warpgroups issued the previous item's last dW
+        if (ni >= 1) mbar_wait_warp(bar_qdofree, (ni - 1) & 1);
+        SB_TR(args, 0, ni, 12);
+        if (leader) {
           for (int w = 0; w < nw; ++w) {
             mbar_expect_tx(bar_do + w, C::kQBytes);
             for (int c = 0; c < D / 64; ++c)
@@ -451,7 +483,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         for (int j = 0; j < it.n_s; ++j, ++jg) {
           const int s = jg % ST;
-          if (jg >= ST) mbar_wait(bar_kempty + s, ((jg / ST) - 1) & 1);
+          if (jg >= ST) mbar_wait_warp(bar_kempty + s, ((jg / ST) - 1) & 1);
           SB_TR(args, 2, jg, 12);
           const int kb = it.kb_lo + j;
           if (leader) {
@@ -478,7 +510,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const Unit& u = it.u;
         for (int j = 0; j < it.n_s; ++j, ++jg) {
           const int s = jg % VST;
-          if (jg >= VST) mbar_wait(bar_vempty + s, ((jg / VST) - 1) & 1);
+          if (jg >= VST) mbar_wait_warp(bar_vempty + s, ((jg / VST) - 1) & 1);
           if (leader) {
             mbar_expect_tx(bar_vfull + s, C::kKVBytes);
             for (int c = 0; c < D / 64; ++c)
@@ -515,9 +547,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (w == 1 && !it.has1) {  // no tile for this warpgroup: release the stream
           for (int j = 0; j < it.n_s; ++j) {
             const int js = jg + j;
-            mbar_wait(bar_kfull + js % ST, (js / ST) & 1);
+            mbar_wait_iss(bar_kfull + js % ST, (js / ST) & 1);
             if (leader) mbar_arrive(bar_kempty + js % ST);
-            mbar_wait(bar_vfull + js % VST, (js / VST) & 1);
+            mbar_wait_iss(bar_vfull + js % VST, (js / VST) & 1);
             if (leader) mbar_arrive(bar_vempty + js % VST);
             __syncwarp();
           }
@@ -530,18 +562,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           continue;
         }
         const int n_w = (w ? it.kbhi1 : it.kbhi0) - it.kb_lo + 1;
-        mbar_wait(bar_do + w, nwi & 1);  // dO of this warpgroup's nwi-th tile (dW reads it)
         // Static issue order: S(j+1) once S(j) was read (it runs while the
-        // warpgroup still works on tile j), dQ(j) once dZ(j) is in smem, dW(j+1)
-        // once dW(j) was read and V(j+1) landed (V is single-buffered).
+        // warpgroup still works on tile j), dW(j+1) once dW(j) was read and V(j+1)
+        // landed, dQ(j) once dZ(j) is in smem.
         auto issue_s = [&](int j) {
           const int js = jg + j, s = js % ST, gi = ig + j;
-          mbar_wait(bar_kfull + s, (js / ST) & 1);
+          mbar_wait_iss(bar_kfull + s, (js / ST) & 1);
           SB_TR(args, 2 + w, gi, 13);
           // the shared S/dW buffer is free once dW(j-1) was read; the item's first S
           // needs this item's Q in TMEM
-          if (gi >= 1) mbar_wait(wempty, (gi - 1) & 1);
-          if (j == 0) mbar_wait(bar_qtm + w, nwi & 1);
+          if (gi >= 1) mbar_wait_iss(wempty, (gi - 1) & 1);
+          if (j == 0) mbar_wait_iss(bar_qtm + w, nwi & 1);
           SB_TR(args, 2 + w, gi, 8);
           tc_fence_after();
           if (leader) {
@@ -556,8 +587,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         };
         auto issue_w = [&](int j) {
           const int js = jg + j, gi = ig + j, sv = js % VST;
-          mbar_wait(bar_vfull + sv, (js / VST) & 1);
-          mbar_wait(sempty, gi & 1);  // S(j) was read out of the shared buffer
+          // (warp-collective: with a one-tile item, this dW's own commit lets the next
+          // dO load complete the barrier's next phase within microseconds)
+          if (j == 0) mbar_wait_warp(bar_do + w, nwi & 1);  // this warpgroup's nwi-th dO tile
+          mbar_wait_iss(bar_vfull + sv, (js / VST) & 1);
+          mbar_wait_iss(sempty, gi & 1);  // S(j) was read out of the shared buffer
           SB_TR(args, 2 + w, gi, 10);
           tc_fence_after();
           if (leader) {
@@ -577,16 +611,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         issue_w(0);
         for (int j = 0; j < n_w; ++j) {
           if (j + 1 < n_w) issue_s(j + 1);
-          // d=64 (K ring 4, V ring 2): dW(j+1) ahead of dQ(j), as soon as dW(j) was read
-          // (C4 phase 1 2.32 -> 2.30 ms); d=128 (K ring 3, one V buffer): after dQ(j),
-          // whose commit frees the K slot (the early order measured 0.915 -> 0.956 ms)
-          constexpr bool kEarlyW = D == 64;
+          // dW(j+1) ahead of dQ(j), as soon as dW(j) was read (C4 phase 1 2.32 -> 2.30 ms;
+          // C2 0.902 -> 0.896; with d=128's former single V buffer the early order was
+          // slower, 0.915 -> 0.956 ms: dW(j+1) then waited for V behind dQ(j))
+#ifndef SB_P1_EARLYW128
+#define SB_P1_EARLYW128 1
+#endif
+          constexpr bool kEarlyW = D == 64 || SB_P1_EARLYW128;
           if (kEarlyW && j + 1 < n_w) issue_w(j + 1);
           const int js = jg + j, s = js % ST, gi = ig + j;
-          mbar_wait(zfull, gi & 1);
+          mbar_wait_iss(zfull, gi & 1);
           SB_TR(args, 2 + w, gi, 11);
           // the previous item's dQ must be out of TMEM before it is overwritten
-          if (j == 0 && nwi >= 1) mbar_wait(dq_free, (nwi - 1) & 1);
+          if (j == 0 && nwi >= 1) mbar_wait_iss(dq_free, (nwi - 1) & 1);
           tc_fence_after();
           if (leader) {
 #pragma unroll
@@ -615,9 +652,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int j = n_w; j < it.n_s; ++j) {  // stream tiles right of this WG's diagonal
           // release each buffer in its own phase: wait until tile j occupies it
           const int js = jg + j;
-          mbar_wait(bar_kfull + js % ST, (js / ST) & 1);
+          mbar_wait_iss(bar_kfull + js % ST, (js / ST) & 1);
           if (leader) mbar_arrive(bar_kempty + js % ST);
-          mbar_wait(bar_vfull + js % VST, (js / VST) & 1);
+          mbar_wait_iss(bar_vfull + js % VST, (js / VST) & 1);
           if (leader) mbar_arrive(bar_vempty + js % VST);
           __syncwarp();
         }
@@ -701,7 +738,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // copy this thread's Q row (TMA-swizzled smem) into TMEM lane r: the A operand of
         // the TS MMA S = Q K^T (as the forward does)
         mbar_wait(bar_qdo + w, nwi & 1);
-        const uint32_t qrow = smem_u32(smem + C::kOffQ + w * C::kQBytes) + r * 128;
+        const uint32_t qrow = smem_u32(smem + C::q_off(w)) + r * 128;
         uint32_t qv[D / 2];
 #pragma unroll
         for (int c = 0; c < D / 8; ++c) {
@@ -1020,7 +1057,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         it.fill(wi.kb0 / 2);
         int qt = it.next();
         if (qt >= u.n_qt) continue;  // nothing visited: the warpgroups write zeros
-        if (ni >= 1) mbar_wait(kv_free, (ni - 1) & 1);
+        if (ni >= 1) mbar_wait_warp(kv_free, (ni - 1) & 1);
         if (leader) {
           // both key blocks; rows past L (odd nb) are zero-filled by the TMA
           mbar_expect_tx(bar_kv, 2 * C::kPairBytes);
@@ -1036,7 +1073,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         for (; qt < u.n_qt; qt = it.next(), ++jg) {
           const int s = jg % ST;
-          if (jg >= ST) mbar_wait(bar_qempty + s, ((jg / ST) - 1) & 1);
+          if (jg >= ST) mbar_wait_warp(bar_qempty + s, ((jg / ST) - 1) & 1);
           SB_TR(args, 2, jg, 12);
           if (leader) {
             uint8_t* qdst = smem + C::kOffQ + s * C::kQBytes;
@@ -1046,7 +1083,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                           u.trow0 + qt * kTileM, wi.h, u.tb);
           }
           __syncwarp();
-          if (jg >= 1) mbar_wait(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
+          if (jg >= 1) mbar_wait_warp(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
           if (leader) {
             mbar_expect_tx(bar_dofull, C::kQBytes);
             for (int c = 0; c < D / 64; ++c)
@@ -1078,9 +1115,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // [dW(j) read], dK(j) [dZ(j) in smem].
       auto issue_s = [&](int jg) {
         const uint32_t qo = (jg % ST) * C::kQBytes;
-        mbar_wait(bar_qfull + jg % ST, (jg / ST) & 1);
+        mbar_wait_iss(bar_qfull + jg % ST, (jg / ST) & 1);
         SB_TR(args, 2, jg, 13);
-        if (jg >= 1) mbar_wait(sempty, (jg - 1) & 1);
+        if (jg >= 1) mbar_wait_iss(sempty, (jg - 1) & 1);
         SB_TR(args, 2, jg, 8);
         tc_fence_after();
         if (leader) {
@@ -1095,8 +1132,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
       };
       auto issue_w = [&](int jg, bool last) {
-        mbar_wait(bar_dofull, jg & 1);
-        if (jg >= 1) mbar_wait(wempty, (jg - 1) & 1);
+        mbar_wait_iss(bar_dofull, jg & 1);
+        if (jg >= 1) mbar_wait_iss(wempty, (jg - 1) & 1);
         SB_TR(args, 2, jg, 10);
         tc_fence_after();
         if (leader) {
@@ -1123,7 +1160,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int n = 0;
         for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
         if (n == 0) continue;
-        mbar_wait(bar_kv, ni & 1);
+        mbar_wait_iss(bar_kv, ni & 1);
         issue_s(jg);
         issue_w(jg, n == 1);
         // Fixed issue order: dV(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1)
@@ -1132,9 +1169,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int j = 0; j < n; ++j, ++jg) {
           const int s = jg % ST;
           const uint32_t qo = s * C::kQBytes;
-          mbar_wait(afull, jg & 1);
+          mbar_wait_iss(afull, jg & 1);
           // the previous item's dV/dK must be out of TMEM before overwriting
-          if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);
+          if (j == 0 && ni >= 1) mbar_wait_iss(acc_free, (ni - 1) & 1);
           SB_TR(args, 2, jg, 9);
           tc_fence_after();
           if (leader) {
@@ -1147,7 +1184,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           __syncwarp();
           if (j + 1 < n) issue_s(jg + 1);
-          mbar_wait(zfull, jg & 1);
+          mbar_wait_iss(zfull, jg & 1);
           SB_TR(args, 2, jg, 11);
           tc_fence_after();
           if (leader) {
@@ -1564,7 +1601,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int qt = it.next();
         if (qt >= u.n_qt) continue;  // nothing visited: the warpgroups write zeros
         if (warp == 8) {
-          if (ni >= 1) mbar_wait(kv_free, (ni - 1) & 1);
+          if (ni >= 1) mbar_wait_warp(kv_free, (ni - 1) & 1);
           if (leader) {
             mbar_expect_tx(bar_kv, C::kPairBytes);
             for (int w = 0; w < 2; ++w)  // the K tensor map has 64-row boxes
@@ -1579,7 +1616,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           prefetch_one();
           if (warp == 8) {
             const int s = jg % ST;
-            if (jg >= ST) mbar_wait(bar_qempty + s, ((jg / ST) - 1) & 1);
+            if (jg >= ST) mbar_wait_warp(bar_qempty + s, ((jg / ST) - 1) & 1);
             SB_TR(args, 3, jg, 0);
             if (leader) {
               mbar_expect_tx(bar_qfull + s, C::kQBytes);
@@ -1590,7 +1627,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
           } else if (warp == 10) {
             const int z = jg & 1;
-            if (jg >= 2) mbar_wait(bar_zempty + z, ((jg >> 1) - 1) & 1);  // dK(jg-2) read dZ
+            if (jg >= 2) mbar_wait_warp(bar_zempty + z, ((jg >> 1) - 1) & 1);  // dK(jg-2) read dZ
             SB_TR(args, 3, jg, 2);
             if (leader) {
 #ifdef SB_NOZ  // tuning ablation: no dZ traffic (dK reads whatever is in the buffer)
@@ -1603,7 +1640,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #endif
             }
           } else {
-            if (jg >= 1) mbar_wait(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
+            if (jg >= 1) mbar_wait_warp(bar_doempty, (jg - 1) & 1);  // dV(jg-1) read dO
             SB_TR(args, 3, jg, 4);
             if (leader) {
               mbar_expect_tx(bar_dofull, C::kQBytes);
@@ -1631,9 +1668,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t qo = (jg % ST) * C::kQBytes;
         const int b = jg & 1;
         SB_TR(args, 2, jg, 0);
-        mbar_wait(bar_qfull + jg % ST, (jg / ST) & 1);
+        mbar_wait_iss(bar_qfull + jg % ST, (jg / ST) & 1);
         SB_TR(args, 2, jg, 1);
-        if (jg >= 2) mbar_wait(sempty + b, ((jg >> 1) - 1) & 1);
+        if (jg >= 2) mbar_wait_iss(sempty + b, ((jg >> 1) - 1) & 1);
         SB_TR(args, 2, jg, 2);
         tc_fence_after();
         if (leader) {
@@ -1660,13 +1697,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int n = 0;
         for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
         if (n == 0) continue;
-        mbar_wait(bar_kv, ni & 1);
+        mbar_wait_iss(bar_kv, ni & 1);
         issue_s(jg, n == 1);
         for (int j = 0; j < n; ++j, ++jg) {
           const int s = jg % ST, z = jg & 1;
-          mbar_wait(bar_zfull + z, (jg >> 1) & 1);
+          mbar_wait_iss(bar_zfull + z, (jg >> 1) & 1);
           SB_TR(args, 2, jg, 7);
-          if (j == 0 && ni >= 1) mbar_wait(acc_free, (ni - 1) & 1);  // epilogue read dK/dV
+          if (j == 0 && ni >= 1) mbar_wait_iss(acc_free, (ni - 1) & 1);  // epilogue read dK/dV
           tc_fence_after();
           if (leader) {
 #pragma unroll
@@ -1680,9 +1717,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // S(j+1) into the other TMEM buffer: it runs while the warpgroups
           // compute A(j)
           if (j + 1 < n) issue_s(jg + 1, j + 2 == n);
-          mbar_wait(afull, jg & 1);
+          mbar_wait_iss(afull, jg & 1);
           SB_TR(args, 2, jg, 4);
-          mbar_wait(bar_dofull, jg & 1);
+          mbar_wait_iss(bar_dofull, jg & 1);
           SB_TR(args, 2, jg, 5);
           tc_fence_after();
           if (leader) {
@@ -1896,3 +1933,9 @@ int bwd_dispatch(int D, const CUtensorMap& tq, const CUtensorMap& tdo, const CUt
 }
 
 }  // namespace sb
+
+#ifdef SB_WATCHDOG_PRINT
+extern "C" int sb_debug_set_wd_bwd(void* p) {
+  return (int)cudaMemcpyToSymbol(sb::g_sb_wd, &p, sizeof(p));
+}
+#endif

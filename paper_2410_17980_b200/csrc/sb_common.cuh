@@ -147,7 +147,7 @@ __device__ __forceinline__ int sched_produce(const SchedRing& q, int k, unsigned
 }
 // consumer warp, k-th item
 __device__ __forceinline__ int sched_consume(const SchedRing& q, int k) {
-  mbar_wait(q.full + (k & 3), (k >> 2) & 1);
+  mbar_wait_warp(q.full + (k & 3), (k >> 2) & 1);  // every consumer is a whole warp
   int idx = 0;
   if ((threadIdx.x & 31) == 0) {
     idx = atomicAdd(q.slot + (k & 3), 0);

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const FwdItem it = fwd_item(g, idx);
       if (!it.valid) continue;
       const Unit& u = it.u;
-      if (ni >= 1) mbar_wait(bar_qfree, (ni - 1) & 1);
+      if (ni >= 1) mbar_wait_warp(bar_qfree, (ni - 1) & 1);
       if (leader) {
         for (int w = 0; w < (it.has1 ? 2 : 1); ++w) {
           mbar_expect_tx(bar_q + w, C::kQBytes);
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         const int s = jg % ST;
         // wait for the slot: it is always freed, also after both warpgroups stopped
         // (their issuers release every loaded tile they no longer read as it lands)
-        if (jg >= ST) mbar_wait(bar_kvempty + s, ((jg / ST) - 1) & 1);
+        if (jg >= ST) mbar_wait_warp(bar_kvempty + s, ((jg / ST) - 1) & 1);
         // skip: stop once both warpgroups are done (their stops are published before
         // they release S; one look per tile, the ring slack absorbs the lag)
         if (kSkip && j > 0 && stop_of(0, ni) <= j && (!it.has1 || stop_of(1, ni) <= j)) {
@@ -261,8 +261,11 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         for (;;) {
           // landed-test first, count second: if the count is not out yet, a landed
           // tile cannot be the next item's (the producer publishes before loading it)
-          const bool kv = mbar_test(bar_kfull + s, par) && mbar_test(bar_vfull + s, par);
-          if (mbar_test(nb_bar, nb_par)) {
+          // warp-uniform decisions (a lane breaking out alone could let the ring slot
+          // complete its next phase before the others poll: see mbar_wait_warp)
+          const bool kv = __any_sync(
+              0xffffffffu, mbar_test(bar_kfull + s, par) && mbar_test(bar_vfull + s, par));
+          if (__any_sync(0xffffffffu, mbar_test(nb_bar, nb_par))) {
             const int n = flag_read(nload_v + (ni & 1));
             if (j >= n) return n;
           }
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         } else {
           for (int j = 0; j < n_rel; ++j) {
             const int js = jg + j;
-            mbar_wait(bar_vfull + js % ST, (js / ST) & 1);
+            mbar_wait_iss(bar_vfull + js % ST, (js / ST) & 1);
             if (leader) mbar_arrive(bar_kvempty + js % ST);
             __syncwarp();
           }
@@ -303,16 +306,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const int n_w = it.n_s - j0;
       // S = Q K^T reads Q from TMEM (copied there by the warpgroup); the smem Q
       // buffer of this warpgroup is free for the next item from then on
-      mbar_wait(bar_qtm + w, nwi & 1);
+      mbar_wait_iss(bar_qtm + w, nwi & 1);
       if (leader) mbar_arrive(bar_qfree);
       __syncwarp();
       auto issue_pv = [&](int i) {  // local tile i == stream tile j0 + i
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
-        mbar_wait(pfull + (gi & 1), (gi >> 1) & 1);
+        mbar_wait_iss(pfull + (gi & 1), (gi >> 1) & 1);
         SB_TR(args, 2 + w, gi, 9);
-        mbar_wait(bar_vfull + s, (js / ST) & 1);
+        mbar_wait_iss(bar_vfull + s, (js / ST) & 1);
         // O of the previous item must be out of TMEM before it is overwritten
-        if (i == 0 && nwi >= 1) mbar_wait(bar_ofree + w, (nwi - 1) & 1);
+        if (i == 0 && nwi >= 1) mbar_wait_iss(bar_ofree + w, (nwi - 1) & 1);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -327,20 +330,20 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       };
       for (int j = 0; j < j0; ++j) {  // stream tiles right of this WG's diagonal
         const int js = jg + j;
-        mbar_wait(bar_vfull + js % ST, (js / ST) & 1);
+        mbar_wait_iss(bar_vfull + js % ST, (js / ST) & 1);
         if (leader) mbar_arrive(bar_kvempty + js % ST);
         __syncwarp();
       }
       int n_proc = n_w;  // tiles this warpgroup processes (skip: up to its stop)
       for (int i = 0; i < n_w; ++i) {
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
-        if (gi >= 1) mbar_wait(sempty, (gi - 1) & 1);  // S is single-buffered
+        if (gi >= 1) mbar_wait_iss(sempty, (gi - 1) & 1);  // S is single-buffered
         // skip: the warpgroup published its stop before releasing S of tile i-1
         if (kSkip && i > 0 && stop_of(w, ni) <= j0 + i) {
           n_proc = i;
           break;
         }
-        mbar_wait(bar_kfull + s, (js / ST) & 1);
+        mbar_wait_iss(bar_kfull + s, (js / ST) & 1);
         SB_TR(args, 2 + w, gi, 8);
         tc_fence_after();
         if (leader) {

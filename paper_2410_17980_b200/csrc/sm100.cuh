@@ -3,6 +3,7 @@
 // -gencode arch=compute_100a,code=sm_100a). No CUTLASS/CuTe dependency.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -74,13 +75,75 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ bool watchdog_expired(long long t0) {
   return SB_WATCHDOG_LOG2 > 0 && clock64() - t0 > (1ll << (SB_WATCHDOG_LOG2 & 63));
 }
+#ifdef SB_WATCHDOG_PRINT
+// debugging build: a timed-out wait records (cta, warp, barrier, parity) in a
+// host-mapped buffer (sb_debug_set_wd_bwd; tools/watchdog_probe.py), which survives
+// the trap that follows
+static __device__ unsigned* g_sb_wd;
+#endif
+// Pending-wait bookkeeping shared by the two waits below: every 1024 polls, trap once
+// 2^SB_WATCHDOG_LOG2 clocks passed (the debugging build records the wait first).
+__device__ __forceinline__ void mbar_watchdog(uint32_t& n, long long t0, uint64_t* bar,
+                                              uint32_t parity) {
+  if ((++n & 1023u) != 0) return;
+#ifdef SB_WATCHDOG_PRINT
+  if (watchdog_expired(t0) || (g_sb_wd && g_sb_wd[1])) {
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(__activemask()) - 1) && g_sb_wd) {
+      atomicExch(g_sb_wd + 1, 1u);
+      const unsigned k = atomicAdd(g_sb_wd, 1u);
+      if (k < 4000) {
+        volatile unsigned* e = g_sb_wd + 4 + 4 * k;
+        e[0] = blockIdx.x;
+        e[1] = (threadIdx.x >> 5) | ((threadIdx.x & 31) << 16);
+        e[2] = smem_u32(bar);
+        e[3] = parity;
+        __threadfence_system();
+      }
+    }
+    // let the other stuck warps record theirs, then fail
+    const long long t1 = clock64();
+    while (!watchdog_expired(t1)) {
+    }
+    __trap();
+  }
+#else
+  (void)bar;
+  (void)parity;
+  if (watchdog_expired(t0)) __trap();
+#endif
+}
+// Per-thread wait: for threads whose barrier cannot complete its next phase without
+// their own later arrival (the stick warpgroups: S, dW, dZ, ... all count every
+// thread), and for a single elected thread.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && watchdog_expired(t0)) __trap();
-  }
+  while (!mbar_try_wait(bar, parity)) mbar_watchdog(n, t0, bar, parity);
+}
+// Warp-collective wait (all 32 lanes call it): the warp leaves together once ANY lane
+// saw the phase complete.  A per-lane wait is not safe in the producer and MMA-issuer
+// warps: their lanes can observe a completion at different polls (they are not kept
+// converged), and once the elected lane moved on, its TMA load or MMA can let the
+// barrier complete its NEXT phase (e.g. the phase-1 Q buffer: load -> the stick
+// warpgroup copies it -> free again, a few microseconds) before a lagging lane polls
+// again; the laggard then sees the parity it waits for as in progress and never
+// returns (C4, many short items per CTA, deadlocked phase 1).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  __syncwarp();
+  if (__any_sync(0xffffffffu, mbar_try_wait(bar, parity))) return;
+  const long long t0 = clock64();
+  uint32_t n = 0;
+  while (!__any_sync(0xffffffffu, mbar_try_wait(bar, parity))) mbar_watchdog(n, t0, bar, parity);
+}
+// MMA-issuer waits: warp-collective with SB_ISSUER_WARP_WAITS, per-lane otherwise (the
+// issuers' other barriers complete their next phase only a full pipeline round later)
+__device__ __forceinline__ void mbar_wait_iss(uint64_t* bar, uint32_t parity) {
+#ifdef SB_ISSUER_WARP_WAITS
+  mbar_wait_warp(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 
 // ---------------------------------------------------------------- fences / barriers

@@ -71,6 +71,24 @@ def main():
             print(f"  role {role}: {len(rows)} tiles")
             for j, ev in rows[:6] + rows[-2:]:
                 print(f"    j={j:2d} " + " ".join(f"{e:7d}" for e in ev[:14]))
+    if a.phase == 2:
+        # store-mode phase 2 (sb_bwd_kvs_kernel): stick warpgroups 0 start, 1 S landed,
+        # 2 A computed, 3 aused (dV(j-1) read A), 4 A stored; MMA issuer (role 2) 7 dZ
+        # landed, 0/1 Q(j+1) wait, 2 S buffer free, 4 A full, 5 dO landed
+        for role, order in ((0, [0, 1, 2, 3, 4]), (1, [0, 1, 2, 3, 4]), (2, [7, 0, 1, 2, 4, 5])):
+            d = {f"{x}->{y}": [] for x, y in zip(order, order[1:])}
+            per_tile = []
+            for c in range(NCTA):
+                for j in range(1, NT - 1):
+                    ev, nx = t[c, role, j], t[c, role, j + 1]
+                    if not all(ev[e] for e in order):
+                        continue
+                    for x, y in zip(order, order[1:]):
+                        d[f"{x}->{y}"].append(int(ev[y] - ev[x]))
+                    if nx[order[0]]:
+                        per_tile.append(int(nx[order[0]] - ev[order[0]]))
+            print(f"role {role} median clk:", {k: int(np.median(v)) for k, v in d.items() if v},
+                  "tile:", int(np.median(per_tile)) if per_tile else None)
     if a.phase == 1:
         # median clocks between the stick warpgroups' per-tile events (tiles j >= 1 of
         # every traced CTA/role): 0 start, 1 S loaded, 7 turn taken, 8 pass 1 done,
