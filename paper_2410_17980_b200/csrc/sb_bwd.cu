@@ -451,9 +451,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int i = 0; i < nw; ++i) {
           const int w = C::kQBufs == 2 ? i : nw - 1 - i;
           const int prev = C::kQBufs == 2 ? w : qlast;
-#ifdef SB_QLATE64
-          if (C::kQBufs == 2 && ni >= 1) mbar_wait_warp(bar_qdofree, (ni - 1) & 1);
-#endif
           if (prev >= 0 && nq[prev] >= 1) mbar_wait_warp(bar_qtm + prev, (nq[prev] - 1) & 1);
           if (leader) {
             mbar_expect_tx(bar_qdo + w, C::kQBytes);
@@ -547,9 +544,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (w == 1 && !it.has1) {  // no tile for this warpgroup: release the stream
           for (int j = 0; j < it.n_s; ++j) {
             const int js = jg + j;
-            mbar_wait_iss(bar_kfull + js % ST, (js / ST) & 1);
+            mbar_wait_warp(bar_kfull + js % ST, (js / ST) & 1);
             if (leader) mbar_arrive(bar_kempty + js % ST);
-            mbar_wait_iss(bar_vfull + js % VST, (js / VST) & 1);
+            mbar_wait_warp(bar_vfull + js % VST, (js / VST) & 1);
             if (leader) mbar_arrive(bar_vempty + js % VST);
             __syncwarp();
           }
@@ -567,12 +564,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // landed, dQ(j) once dZ(j) is in smem.
         auto issue_s = [&](int j) {
           const int js = jg + j, s = js % ST, gi = ig + j;
-          mbar_wait_iss(bar_kfull + s, (js / ST) & 1);
+          mbar_wait_warp(bar_kfull + s, (js / ST) & 1);
           SB_TR(args, 2 + w, gi, 13);
           // the shared S/dW buffer is free once dW(j-1) was read; the item's first S
           // needs this item's Q in TMEM
-          if (gi >= 1) mbar_wait_iss(wempty, (gi - 1) & 1);
-          if (j == 0) mbar_wait_iss(bar_qtm + w, nwi & 1);
+          if (gi >= 1) mbar_wait_warp(wempty, (gi - 1) & 1);
+          if (j == 0) mbar_wait_warp(bar_qtm + w, nwi & 1);
           SB_TR(args, 2 + w, gi, 8);
           tc_fence_after();
           if (leader) {
@@ -587,11 +584,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         };
         auto issue_w = [&](int j) {
           const int js = jg + j, gi = ig + j, sv = js % VST;
-          // (warp-collective: with a one-tile item, this dW's own commit lets the next
-          // dO load complete the barrier's next phase within microseconds)
           if (j == 0) mbar_wait_warp(bar_do + w, nwi & 1);  // this warpgroup's nwi-th dO tile
-          mbar_wait_iss(bar_vfull + sv, (js / VST) & 1);
-          mbar_wait_iss(sempty, gi & 1);  // S(j) was read out of the shared buffer
+          mbar_wait_warp(bar_vfull + sv, (js / VST) & 1);
+          mbar_wait_warp(sempty, gi & 1);  // S(j) was read out of the shared buffer
           SB_TR(args, 2 + w, gi, 10);
           tc_fence_after();
           if (leader) {
@@ -620,10 +615,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           constexpr bool kEarlyW = D == 64 || SB_P1_EARLYW128;
           if (kEarlyW && j + 1 < n_w) issue_w(j + 1);
           const int js = jg + j, s = js % ST, gi = ig + j;
-          mbar_wait_iss(zfull, gi & 1);
+          mbar_wait_warp(zfull, gi & 1);
           SB_TR(args, 2 + w, gi, 11);
           // the previous item's dQ must be out of TMEM before it is overwritten
-          if (j == 0 && nwi >= 1) mbar_wait_iss(dq_free, (nwi - 1) & 1);
+          if (j == 0 && nwi >= 1) mbar_wait_warp(dq_free, (nwi - 1) & 1);
           tc_fence_after();
           if (leader) {
 #pragma unroll
@@ -652,9 +647,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int j = n_w; j < it.n_s; ++j) {  // stream tiles right of this WG's diagonal
           // release each buffer in its own phase: wait until tile j occupies it
           const int js = jg + j;
-          mbar_wait_iss(bar_kfull + js % ST, (js / ST) & 1);
+          mbar_wait_warp(bar_kfull + js % ST, (js / ST) & 1);
           if (leader) mbar_arrive(bar_kempty + js % ST);
-          mbar_wait_iss(bar_vfull + js % VST, (js / VST) & 1);
+          mbar_wait_warp(bar_vfull + js % VST, (js / VST) & 1);
           if (leader) mbar_arrive(bar_vempty + js % VST);
           __syncwarp();
         }
@@ -1115,9 +1110,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // [dW(j) read], dK(j) [dZ(j) in smem].
       auto issue_s = [&](int jg) {
         const uint32_t qo = (jg % ST) * C::kQBytes;
-        mbar_wait_iss(bar_qfull + jg % ST, (jg / ST) & 1);
+        mbar_wait_warp(bar_qfull + jg % ST, (jg / ST) & 1);
         SB_TR(args, 2, jg, 13);
-        if (jg >= 1) mbar_wait_iss(sempty, (jg - 1) & 1);
+        if (jg >= 1) mbar_wait_warp(sempty, (jg - 1) & 1);
         SB_TR(args, 2, jg, 8);
         tc_fence_after();
         if (leader) {
@@ -1132,8 +1127,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
       };
       auto issue_w = [&](int jg, bool last) {
-        mbar_wait_iss(bar_dofull, jg & 1);
-        if (jg >= 1) mbar_wait_iss(wempty, (jg - 1) & 1);
+        mbar_wait_warp(bar_dofull, jg & 1);
+        if (jg >= 1) mbar_wait_warp(wempty, (jg - 1) & 1);
         SB_TR(args, 2, jg, 10);
         tc_fence_after();
         if (leader) {
@@ -1160,7 +1155,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int n = 0;
         for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
         if (n == 0) continue;
-        mbar_wait_iss(bar_kv, ni & 1);
+        mbar_wait_warp(bar_kv, ni & 1);
         issue_s(jg);
         issue_w(jg, n == 1);
         // Fixed issue order: dV(j) [A(j) in smem], S(j+1) [S(j) read, Q(j+1)
@@ -1169,9 +1164,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int j = 0; j < n; ++j, ++jg) {
           const int s = jg % ST;
           const uint32_t qo = s * C::kQBytes;
-          mbar_wait_iss(afull, jg & 1);
+          mbar_wait_warp(afull, jg & 1);
           // the previous item's dV/dK must be out of TMEM before overwriting
-          if (j == 0 && ni >= 1) mbar_wait_iss(acc_free, (ni - 1) & 1);
+          if (j == 0 && ni >= 1) mbar_wait_warp(acc_free, (ni - 1) & 1);
           SB_TR(args, 2, jg, 9);
           tc_fence_after();
           if (leader) {
@@ -1184,7 +1179,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           __syncwarp();
           if (j + 1 < n) issue_s(jg + 1);
-          mbar_wait_iss(zfull, jg & 1);
+          mbar_wait_warp(zfull, jg & 1);
           SB_TR(args, 2, jg, 11);
           tc_fence_after();
           if (leader) {
@@ -1668,9 +1663,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t qo = (jg % ST) * C::kQBytes;
         const int b = jg & 1;
         SB_TR(args, 2, jg, 0);
-        mbar_wait_iss(bar_qfull + jg % ST, (jg / ST) & 1);
+        mbar_wait_warp(bar_qfull + jg % ST, (jg / ST) & 1);
         SB_TR(args, 2, jg, 1);
-        if (jg >= 2) mbar_wait_iss(sempty + b, ((jg >> 1) - 1) & 1);
+        if (jg >= 2) mbar_wait_warp(sempty + b, ((jg >> 1) - 1) & 1);
         SB_TR(args, 2, jg, 2);
         tc_fence_after();
         if (leader) {
@@ -1697,13 +1692,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         int n = 0;
         for (int qt = it.next(); qt < u.n_qt; qt = it.next()) ++n;
         if (n == 0) continue;
-        mbar_wait_iss(bar_kv, ni & 1);
+        mbar_wait_warp(bar_kv, ni & 1);
         issue_s(jg, n == 1);
         for (int j = 0; j < n; ++j, ++jg) {
           const int s = jg % ST, z = jg & 1;
-          mbar_wait_iss(bar_zfull + z, (jg >> 1) & 1);
+          mbar_wait_warp(bar_zfull + z, (jg >> 1) & 1);
           SB_TR(args, 2, jg, 7);
-          if (j == 0 && ni >= 1) mbar_wait_iss(acc_free, (ni - 1) & 1);  // epilogue read dK/dV
+          if (j == 0 && ni >= 1) mbar_wait_warp(acc_free, (ni - 1) & 1);  // epilogue read dK/dV
           tc_fence_after();
           if (leader) {
 #pragma unroll
@@ -1717,9 +1712,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // S(j+1) into the other TMEM buffer: it runs while the warpgroups
           // compute A(j)
           if (j + 1 < n) issue_s(jg + 1, j + 2 == n);
-          mbar_wait_iss(afull, jg & 1);
+          mbar_wait_warp(afull, jg & 1);
           SB_TR(args, 2, jg, 4);
-          mbar_wait_iss(bar_dofull, jg & 1);
+          mbar_wait_warp(bar_dofull, jg & 1);
           SB_TR(args, 2, jg, 5);
           tc_fence_after();
           if (leader) {

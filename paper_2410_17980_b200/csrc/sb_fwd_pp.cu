@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         } else {
           for (int j = 0; j < n_rel; ++j) {
             const int js = jg + j;
-            mbar_wait_iss(bar_vfull + js % ST, (js / ST) & 1);
+            mbar_wait_warp(bar_vfull + js % ST, (js / ST) & 1);
             if (leader) mbar_arrive(bar_kvempty + js % ST);
             __syncwarp();
           }
@@ -306,16 +306,16 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       const int n_w = it.n_s - j0;
       // S = Q K^T reads Q from TMEM (copied there by the warpgroup); the smem Q
       // buffer of this warpgroup is free for the next item from then on
-      mbar_wait_iss(bar_qtm + w, nwi & 1);
+      mbar_wait_warp(bar_qtm + w, nwi & 1);
       if (leader) mbar_arrive(bar_qfree);
       __syncwarp();
       auto issue_pv = [&](int i) {  // local tile i == stream tile j0 + i
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
-        mbar_wait_iss(pfull + (gi & 1), (gi >> 1) & 1);
+        mbar_wait_warp(pfull + (gi & 1), (gi >> 1) & 1);
         SB_TR(args, 2 + w, gi, 9);
-        mbar_wait_iss(bar_vfull + s, (js / ST) & 1);
+        mbar_wait_warp(bar_vfull + s, (js / ST) & 1);
         // O of the previous item must be out of TMEM before it is overwritten
-        if (i == 0 && nwi >= 1) mbar_wait_iss(bar_ofree + w, (nwi - 1) & 1);
+        if (i == 0 && nwi >= 1) mbar_wait_warp(bar_ofree + w, (nwi - 1) & 1);
         tc_fence_after();
         if (leader) {
 #pragma unroll
@@ -330,20 +330,20 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       };
       for (int j = 0; j < j0; ++j) {  // stream tiles right of this WG's diagonal
         const int js = jg + j;
-        mbar_wait_iss(bar_vfull + js % ST, (js / ST) & 1);
+        mbar_wait_warp(bar_vfull + js % ST, (js / ST) & 1);
         if (leader) mbar_arrive(bar_kvempty + js % ST);
         __syncwarp();
       }
       int n_proc = n_w;  // tiles this warpgroup processes (skip: up to its stop)
       for (int i = 0; i < n_w; ++i) {
         const int js = jg + j0 + i, s = js % ST, gi = ig + i;
-        if (gi >= 1) mbar_wait_iss(sempty, (gi - 1) & 1);  // S is single-buffered
+        if (gi >= 1) mbar_wait_warp(sempty, (gi - 1) & 1);  // S is single-buffered
         // skip: the warpgroup published its stop before releasing S of tile i-1
         if (kSkip && i > 0 && stop_of(w, ni) <= j0 + i) {
           n_proc = i;
           break;
         }
-        mbar_wait_iss(bar_kfull + s, (js / ST) & 1);
+        mbar_wait_warp(bar_kfull + s, (js / ST) & 1);
         SB_TR(args, 2 + w, gi, 8);
         tc_fence_after();
         if (leader) {

@@ -121,29 +121,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) mbar_watchdog(n, t0, bar, parity);
 }
-// Warp-collective wait (all 32 lanes call it): the warp leaves together once ANY lane
-// saw the phase complete.  A per-lane wait is not safe in the producer and MMA-issuer
-// warps: their lanes can observe a completion at different polls (they are not kept
-// converged), and once the elected lane moved on, its TMA load or MMA can let the
-// barrier complete its NEXT phase (e.g. the phase-1 Q buffer: load -> the stick
-// warpgroup copies it -> free again, a few microseconds) before a lagging lane polls
-// again; the laggard then sees the parity it waits for as in progress and never
-// returns (C4, many short items per CTA, deadlocked phase 1).
+// Warp-collective wait (all 32 lanes call it): no lane returns before every lane saw
+// the phase complete.  A plain per-lane wait is not safe in the producer and
+// MMA-issuer warps: their lanes can observe a completion at different polls (a lane
+// suspended in try_wait may resume late), and once the elected lane moved on, its TMA
+// load or MMA commit can let the barrier complete its NEXT phase (e.g. the phase-1 Q
+// buffer: load -> the stick warpgroup copies it -> free again, a few microseconds)
+// before a lagging lane polls again; the laggard then sees the parity it waits for as
+// in progress and never returns (C4, many short items per CTA, deadlocked phase 1).
+// With the __syncwarp the elected lane cannot act before the last lane has returned.
+// (A vote-per-poll variant cost 3% more on C4's phase 1.)
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
-  __syncwarp();
-  if (__any_sync(0xffffffffu, mbar_try_wait(bar, parity))) return;
-  const long long t0 = clock64();
-  uint32_t n = 0;
-  while (!__any_sync(0xffffffffu, mbar_try_wait(bar, parity))) mbar_watchdog(n, t0, bar, parity);
-}
-// MMA-issuer waits: warp-collective with SB_ISSUER_WARP_WAITS, per-lane otherwise (the
-// issuers' other barriers complete their next phase only a full pipeline round later)
-__device__ __forceinline__ void mbar_wait_iss(uint64_t* bar, uint32_t parity) {
-#ifdef SB_ISSUER_WARP_WAITS
-  mbar_wait_warp(bar, parity);
-#else
   mbar_wait(bar, parity);
-#endif
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- fences / barriers
