@@ -289,16 +289,23 @@ struct BwdQCfg {
   // Q only stages the copy into TMEM at the item start: d = 128 keeps ONE Q buffer that
   // the two warpgroups' tiles take in turn, which makes room for a second V stage and a
   // fourth K stage (C2 phase 1 0.909 -> 0.896 ms with dW(j+1) issued ahead of dQ(j);
-  // V ring 2 alone 0.902); d = 64 has room for a Q buffer per warpgroup, a K ring of 4
-  // and the V ring (C4 phase 1: 2.33 -> 2.31 ms)
+  // V ring 2 alone 0.902); d = 64 has room for a Q buffer per warpgroup, a K ring of 6
+  // and a V ring of 3 (C4 phase 1: K 3 / V 1 2.33 -> K 4 / V 2 2.31 (round 1) ->
+  // K 6 / V 3 2.353 -> 2.311 ms in one A/B; K 8 did not help)
 #ifndef SB_P1_KST128
 #define SB_P1_KST128 4
 #endif
 #ifndef SB_P1_VST128
 #define SB_P1_VST128 2
 #endif
-  static constexpr int kStages = D == 64 ? 4 : SB_P1_KST128;   // K ring
-  static constexpr int kVStages = D == 64 ? 2 : SB_P1_VST128;  // V ring (its own producer warp)
+#ifndef SB_P1_KST64
+#define SB_P1_KST64 6
+#endif
+#ifndef SB_P1_VST64
+#define SB_P1_VST64 3
+#endif
+  static constexpr int kStages = D == 64 ? SB_P1_KST64 : SB_P1_KST128;   // K ring
+  static constexpr int kVStages = D == 64 ? SB_P1_VST64 : SB_P1_VST128;  // V ring (own producer)
   static constexpr int kQBufs = D == 64 ? 2 : (SB_P1_VST128 > 1 ? 1 : 2);
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kKVBytes = kBlock * D * 2;
@@ -1461,7 +1468,12 @@ struct KVCursor {
 
 template <int D>
 struct BwdKVSCfg {
-  static constexpr int kStages = 2;                       // Q ring
+  // Q ring: 2 stages fill the 227 KB at d = 128; d = 64 has room for 4 (C4 phase 2
+  // 2.071 -> 2.045 ms; 3 stages 2.058)
+#ifndef SB_P2_QST64
+#define SB_P2_QST64 4
+#endif
+  static constexpr int kStages = D == 64 ? SB_P2_QST64 : 2;
   static constexpr int kQBytes = kTileM * D * 2;
   static constexpr int kPairBytes = 2 * kBlock * D * 2;  // K of both key blocks
   static constexpr int kPBytes = kTileM * kBlock * 2;    // A / dZ of one key block
