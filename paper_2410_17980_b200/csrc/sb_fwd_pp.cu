@@ -433,6 +433,11 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
       int lowest = my_qb, visited = 0, n_proc = n_w;
       bool my_vote = false;  // skip: this warp's latest vote (all its rows below log eps)
       const int j0 = it.kbhi1 - kbhi;  // stream index of this warpgroup's first tile
+      // d = 64, skip off: P(i)'s fence and `pfull` move into tile i+1, behind its S load
+      // (C4 forward 1.770 -> 1.733 ms).  Not at d = 128: there the issuer then queues the
+      // longer P.V(i) right before S(i+1) (C2 forward 0.617 -> 0.690 ms); not skip on,
+      // whose tiles can end an item early.
+      constexpr bool kDeferP = !kSkip && D == 64;
       for (int i = 0; i < n_w; ++i) {
         const int kb = kbhi - i, gi = ig + i;
         if (tr) SB_TR(args, w, gi, 0);
@@ -441,6 +446,12 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         float s[64];
         tmem_ld32(tS, s);
         tmem_ld32(tS + 32, s + 32);
+        if (kDeferP && i > 0) {
+          // the previous tile's P: its proxy fence waits for the shared stores while
+          // this tile's S is in flight from TMEM
+          fence_proxy_async_smem();
+          mbar_arrive(pfull + ((gi - 1) & 1));
+        }
         tmem_wait_ld();
         if (tr) SB_TR(args, w, gi, 1);
         uint32_t pk[32];
@@ -574,8 +585,10 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
         for (int c = 0; c < 8; ++c)
           st_shared_v4(pb + ((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
                        pk[4 * c + 3]);
-        fence_proxy_async_smem();
-        mbar_arrive(pfull + (gi & 1));
+        if (!kDeferP) {
+          fence_proxy_async_smem();
+          mbar_arrive(pfull + (gi & 1));
+        }
         if (tr) SB_TR(args, w, gi, 4);
         if (kSkip && !done) {
           // the row total of lt for the skip decisions (blocked.py:175-176), after the
@@ -594,6 +607,10 @@ __global__ void __launch_bounds__(FwdPPCfg<D>::kThreads, 1)
           }
         }
         if (done) break;
+      }
+      if (kDeferP) {  // the item's last P
+        fence_proxy_async_smem();
+        mbar_arrive(pfull + ((ig + n_w - 1) & 1));
       }
       // epilogue: O rows leave in 64-column halves through this warp's 4 KB slice
       // of the (now idle: ofull) P buffers as coalesced row segments
