@@ -109,6 +109,23 @@ def main():
                         per_tile.append(int(nxt - ev[0]))
         print("median clk:", {k: int(np.median(v)) for k, v in d.items() if v},
               "tile:", int(np.median(per_tile)) if per_tile else None)
+        # MMA round trips per warpgroup tile (issuer role 2 + w, stick role w): S issued
+        # -> S loaded, dW(j-1) read -> S(j) issued, dW issued -> dW read, dZ stored -> dQ issued
+        x = {"S issue->loaded": [], "dW(j-1) read->S(j) issue": [], "dW issue->read": [],
+             "dZ stored->dQ issue": []}
+        for c in range(NCTA):
+            for w in (0, 1):
+                st, iss = t[c, w], t[c, 2 + w]
+                for j in range(1, NT):
+                    if st[j, 1] and iss[j, 8]:
+                        x["S issue->loaded"].append(int(st[j, 1] - iss[j, 8]))
+                    if iss[j, 8] and st[j - 1, 3]:
+                        x["dW(j-1) read->S(j) issue"].append(int(iss[j, 8] - st[j - 1, 3]))
+                    if st[j, 3] and iss[j, 10]:
+                        x["dW issue->read"].append(int(st[j, 3] - iss[j, 10]))
+                    if iss[j, 11] and st[j, 6]:
+                        x["dZ stored->dQ issue"].append(int(iss[j, 11] - st[j, 6]))
+        print("median clk:", {k: int(np.median(v)) for k, v in x.items() if v})
 
 
 if __name__ == "__main__":
