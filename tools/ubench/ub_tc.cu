@@ -12,6 +12,8 @@ constexpr int ITER = 256;
 
 // mode 0: TMEM loads only (nld warps); 1: MMA only; 2: MMA + TMEM loads
 // mma_kind: 0 = 128x64 K-major (S), 1 = 128x64 MN-major A/B (dV^T), 2 = 128x128 K-major, 3 = 128x256
+// ...; 8 = 128x64 TS (A from TMEM columns 256.., B K-major: phase 1's and the forward's S),
+// 9 = 128x128 TS
 __global__ void __launch_bounds__(544, 1) ub(int mode, int mma_kind, int nld, unsigned long long* out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -30,8 +32,9 @@ __global__ void __launch_bounds__(544, 1) ub(int mode, int mma_kind, int nld, un
     if (lane == 0 && mode >= 1) {
       const uint32_t a = smem_u32(smem), b = smem_u32(smem + 64 * 1024);
       // kinds 0-3: one accumulator; 4: N=64 over 4 accumulators; 5: N=128 over 2; 6: N=256 over 2
-      const int N = (mma_kind == 2 || mma_kind == 5 || mma_kind == 7) ? 128
+      const int N = (mma_kind == 2 || mma_kind == 5 || mma_kind == 7 || mma_kind == 9) ? 128
                     : (mma_kind == 3 || mma_kind == 6) ? 256 : 64;
+      const bool ts = mma_kind >= 8;
       const bool mn = mma_kind == 1 || mma_kind == 7;
       const int nacc = mma_kind == 4 ? 4 : (mma_kind >= 5 ? 2 : 1);
       const uint32_t idesc = idesc_bf16(128, N, mn, mn);
@@ -44,8 +47,13 @@ __global__ void __launch_bounds__(544, 1) ub(int mode, int mma_kind, int nld, un
       const uint32_t cstep = mma_kind == 6 ? 256 : N;
       for (int it = 0; it < ITER; ++it) {
         const uint32_t d = tb + (it % nacc) * cstep;
+        if (ts) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) umma_ss(d, ad[k], bd[k], idesc, 1);
+          for (int k = 0; k < 8; ++k) umma_ts_at(d, tb + 256 + k * 8, bd[0], 0, idesc, 1);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) umma_ss(d, ad[k], bd[k], idesc, 1);
+        }
       }
       umma_commit(bar);
       mbar_wait(bar, 0);
@@ -81,8 +89,9 @@ int main() {
   cudaMalloc(&d, 148 * 2 * 8);
   cudaFuncSetAttribute(ub, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
   const char* kn[] = {"128x64 K-major", "128x64 MN-major", "128x128 K-major", "128x256 K-major",
-                      "128x64 4 acc", "128x128 2 acc", "128x256 2 acc", "128x128 MN/MN"};
-  const int Ns[] = {64, 64, 128, 256, 64, 128, 256, 128};
+                      "128x64 4 acc", "128x128 2 acc", "128x256 2 acc", "128x128 MN/MN",
+                      "128x64 TS", "128x128 TS"};
+  const int Ns[] = {64, 64, 128, 256, 64, 128, 256, 128, 64, 128};
   std::vector<unsigned long long> h(296);
   auto run = [&](int mode, int kind, int nld) {
     cudaMemset(d, 0, 296 * 8);
@@ -109,7 +118,7 @@ int main() {
     printf("\n");
   };
   for (int nld : {4, 8, 16}) run(0, 0, nld);
-  for (int k = 0; k < 8; ++k) run(1, k, 0);
+  for (int k = 0; k < 10; ++k) run(1, k, 0);
   for (int nld : {4, 8}) run(2, 0, nld);
   run(2, 1, 8);
   for (int nld : {4, 8, 16}) run(3, 2, nld);
