@@ -115,8 +115,15 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(t):
+    """The current stream of t's device (not of the current device)."""
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _on(t):
+    """Run a C-ABI call with t's device current: the library sizes grids, sets kernel
+    attributes and launches on the current device, which must own the stream."""
+    return torch.cuda.device(t.device)
 
 
 def _check_qkv(q, k, v, varlen=False):
@@ -235,8 +242,10 @@ def _blocked_forward_varlen(q, k, v, cu_seqlens, skip, skip_eps, scale, counters
     state = _state_tensor(lib, p, q.device) if two_phase else None
     cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
     if max_L > 0:
-        _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
-                              _ptr(first_kb), _ptr(state), _ptr(cnt), _stream()))
+        with _on(q):
+            _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                  _ptr(log_rem), _ptr(first_kb), _ptr(state), _ptr(cnt),
+                                  _stream(q)))
     else:
         o.zero_()
         log_rem.zero_()
@@ -296,8 +305,9 @@ def blocked_forward(q, k, v, layout: BlockLayout | None = None, skip: bool = Fal
     first_kb = torch.empty((B, H, layout.n_blocks), device=q.device, dtype=torch.int32)
     state = _state_tensor(lib, p, q.device) if two_phase else None
     cnt = torch.zeros(2, device=q.device, dtype=torch.int64) if counters else None
-    _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
-                          _ptr(first_kb), _ptr(state), _ptr(cnt), _stream()))
+    with _on(q):
+        _lib.check(lib.sb_fwd(ctypes.byref(p), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(log_rem),
+                              _ptr(first_kb), _ptr(state), _ptr(cnt), _stream(q)))
     total = B * H * layout.n_tiles
     visited = int(cnt[0].item()) if counters else -1
     stats = TileStats(total, visited, total - visited if counters else -1, first_kb)
@@ -532,9 +542,10 @@ def _backward_call(lib, cache, d_o, ro, dq, dk, dv, store, phases, chunk, worksp
     st_ptr = ctypes.c_void_p(state.data_ptr() + 8 * st_off)
     ro_ptr = None if ro is None else ctypes.c_void_p(ro.data_ptr() + 4 * ro_off)
     fkb_ptr = ctypes.c_void_p(fkb.data_ptr() + 4 * fkb_off)
-    _lib.check(lib.sb_bwd(ctypes.byref(p), _ptr(qv), _ptr(kv), _ptr(vv), _ptr(dov), ro_ptr,
-                          st_ptr, fkb_ptr, _ptr(dqv), _ptr(dkv), _ptr(dvv), _ptr(ws),
-                          ws.numel(), host, int(store), int(phases), _stream()))
+    with _on(qv):
+        _lib.check(lib.sb_bwd(ctypes.byref(p), _ptr(qv), _ptr(kv), _ptr(vv), _ptr(dov), ro_ptr,
+                              st_ptr, fkb_ptr, _ptr(dqv), _ptr(dkv), _ptr(dvv), _ptr(ws),
+                              ws.numel(), host, int(store), int(phases), _stream(qv)))
 
 
 class _StickBreakingFn(torch.autograd.Function):
