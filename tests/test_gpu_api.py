@@ -190,3 +190,45 @@ def test_rem_gradient_only_when_requested():
     ref = oracle_fwd(q, k, v)
     np.testing.assert_allclose(rem.detach().cpu().double().numpy(), np.exp(ref["log_rem"]),
                                atol=TOL, rtol=TOL)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_cuda_graph_capture_fwd_bwd(d):
+    """The op (forward + two-phase backward through autograd) captures into one CUDA
+    graph: no host synchronisation or allocation outside torch's graph pool on the
+    path; replays give the eager results bit for bit, also on new inputs copied into
+    the static buffers (launch-bound small shapes can replay a whole step)."""
+    import paper_2410_17980_b200 as sb
+    B, H, L = 2, 4, 384
+    q, k, v, do = make_qkv(B, H, L, d, seed=5)
+
+    def eager(q, k, v, do):
+        qq, kk, vv = (x.detach().clone().requires_grad_(True) for x in (q, k, v))
+        o = sb.stickbreaking_attention(qq, kk, vv)
+        o.backward(do)
+        return [o.detach(), qq.grad, kk.grad, vv.grad]
+
+    sq, sk, sv = (x.detach().clone().requires_grad_(True) for x in (q, k, v))
+    sdo = do.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up (kernel attributes, allocator) off the capture
+        for _ in range(2):
+            sb.stickbreaking_attention(sq, sk, sv).backward(sdo)
+            for x in (sq, sk, sv):
+                x.grad = None
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        so = sb.stickbreaking_attention(sq, sk, sv)
+        so.backward(sdo)
+    for seed in (5, 6):
+        q2, k2, v2, do2 = make_qkv(B, H, L, d, seed=seed)
+        with torch.no_grad():
+            for dst, src in zip((sq, sk, sv, sdo), (q2, k2, v2, do2)):
+                dst.copy_(src)
+        g.replay()
+        torch.cuda.synchronize()
+        ref = eager(q2, k2, v2, do2)
+        for a, b in zip([so.detach(), sq.grad, sk.grad, sv.grad], ref):
+            assert torch.equal(a, b)
